@@ -1,0 +1,384 @@
+"""Benchmark: PN-correlation channel estimation at 64x64 MIMO, PN 1023 (BASELINE cfg3).
+
+One step = one pass of the hot path (pack -> tcgen05 correlate -> fused 1/M + demux)
+over a batch of F frame-sets already resident in HBM (default F = 10,000, the
+BASELINE headline: 47 GB of received IQ, far larger than L2).  value = CSI
+estimates/s = link CIRs (frame, rx, tx) per second over all ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun each rank estimates its own F frame-sets (weak scaling, no
+hot-path collective); the step time is the max over ranks (NCCL all_reduce MAX of
+the CUDA-event time) and the per-rank error statistics are all_reduced at the end.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs[2] (headline single-GPU bench)
+WORKLOAD = dict(name="cfg3", n_t=64, n_r=64, m=1023, l=64, c=64, n_batch=8, snr_db=10.0)
+METRIC = "CSI estimates/sec & us/frame at 64x64 MIMO, PN 1023; tensor-pipe % of peak"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), float(pk["bf16_tflops"]), float(pk.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def algorithmic_per_frame(w):
+    """FLOP = 4*macs (macs = n_t*L*M*n_r), bytes = fp16 body in + c64 taps out."""
+    n_batches = -(-w["n_t"] // w["n_batch"])
+    macs = w["n_t"] * w["l"] * w["m"] * w["n_r"]
+    flop = 4 * macs
+    bytes_gemm = w["n_r"] * n_batches * w["m"] * 2 * 2 + w["n_r"] * w["n_t"] * w["l"] * 8
+    samples = w["c"] + w["m"] + w["l"] - 1
+    bytes_pack = w["n_r"] * n_batches * samples * 8 + w["n_r"] * n_batches * 2 * (-(-w["m"] // 64) * 64) * 2
+    return flop, bytes_gemm, bytes_pack
+
+
+class ClockSampler:
+    """Samples nvidia-smi SM clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if r[4 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def synth_iq_pool(corr, n_pool, w, seed, dev):
+    """Statistically equivalent synthetic received IQ on the device (input synthesis only,
+    not timed): per-link channels with the draw_channel law (channel.py:96-108), the
+    noiseless CP-stripped body H.A (the circulant rows of the plan's own chips), CP =
+    body tail, AWGN at the configured SNR (channel.py:145-183)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    n_t, n_r, l, m, c, nb = w["n_t"], w["n_r"], w["l"], w["m"], w["c"], w["n_batch"]
+    n_batches = -(-n_t // nb)
+    chips = corr.chips().double()
+    spacing = m // nb
+    lags = torch.tensor([(spacing * j + q) % m for j in range(nb) for q in range(l)], device=dev)
+    idx = (torch.arange(m, device=dev)[None, :] - lags[:, None]) % m
+    A = chips[idx]                                           # (nb*L, M)
+    amax = math.sqrt(1.0 / (n_t * math.sqrt(l)))
+    amp = amax * (1.0 - torch.rand((n_pool, n_r, n_t, l), generator=g, device=dev, dtype=torch.float64))
+    ph = 2 * math.pi * torch.rand((n_pool, n_r, n_t, l), generator=g, device=dev, dtype=torch.float64)
+    h = torch.polar(amp, ph)                                 # (F, n_r, n_t, L)
+    samples = c + m + l - 1
+    iq = torch.zeros((n_pool, n_batches, n_r, samples, 2), dtype=torch.float32, device=dev)
+    for b in range(n_batches):
+        hb = h[:, :, b * nb:(b + 1) * nb, :].reshape(n_pool, n_r, -1)   # (F, n_r, nb*L)
+        body = hb @ A[:hb.shape[-1]].to(torch.complex128)               # (F, n_r, M)
+        ref = (body.abs() ** 2).mean(dim=(1, 2), keepdim=True) / (nb * l)
+        sigma = torch.sqrt(ref / (10 ** (w["snr_db"] / 10)) / 2)
+        noise = torch.complex(torch.randn(body.shape, generator=g, device=dev, dtype=torch.float64),
+                              torch.randn(body.shape, generator=g, device=dev, dtype=torch.float64))
+        body = body + sigma * noise
+        iq[:, b, :, c:c + m, 0] = body.real.float()
+        iq[:, b, :, c:c + m, 1] = body.imag.float()
+        iq[:, b, :, :c, 0] = body.real[..., m - c:].float()
+        iq[:, b, :, :c, 1] = body.imag[..., m - c:].float()
+    return iq, h.to(torch.complex64)
+
+
+def cpu_reference_rate(w, seconds, threads=None):
+    """Time the oracle port of process_frames (reference64, experiments.py:176-208) on the
+    host cores over a bounded sample; returns (CSI estimates/s, cores, sample description)."""
+    import numpy as np
+    from oracle import pnce_oracle as O
+    cfg = O.Config(m=w["m"], c=w["c"], n_t=w["n_t"], n_batch=w["n_batch"], l=w["l"], n_r=w["n_r"])
+    chips = O.sequence_for_length(w["m"])
+    plan = O.build_batch_plan(cfg)
+    rows = O.correlator_rows_for_plan(chips, plan, cfg.l)
+    # two distinct pre-simulated frame-sets (experiments.py:373: synthesis is untimed)
+    pool = []
+    for it in range(2):
+        cs, ns = O.derive_seeds(0, cfg.m, cfg.n_batch, cfg.l, 0, it)
+        _, frames = O.simulate_frame(chips, cfg, cfg.l, w["snr_db"], cs, ns)
+        pool.append(O.iq_to_frames(O.frames_to_iq(frames)))
+    for f in pool:   # warm-up (run_latency_bench warmup=2)
+        O.process_frames(chips, cfg, f, rows_per_batch=rows)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        f = pool[len(times) % 2]
+        t0 = time.perf_counter()
+        O.process_frames(chips, cfg, f, rows_per_batch=rows)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    cores = threads or os.cpu_count()
+    rate = w["n_r"] * w["n_t"] / med
+    sample = (f"{len(times)} frame-sets of cfg3 through the numpy oracle port of process_frames "
+              f"(reference64), median {med * 1e3:.2f} ms/frame-set, {cores} BLAS threads")
+    return rate, cores, sample, med
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    w = WORKLOAD
+    per_step = []
+    sample = None
+    cores = os.cpu_count()
+    for i in range(args.warmup + args.steps):
+        rate, cores, sample, med = cpu_reference_rate(w, seconds=args.ref_seconds)
+        if i >= args.warmup:
+            per_step.append(med)
+    med = statistics.median(per_step)
+    value = w["n_r"] * w["n_t"] / med
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "CSI estimates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "us_per_frame": med * 1e6, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8, 10 dB",
+                   "frames_per_step": 1, "parallelism": "host threads (OpenBLAS)"},
+        "cpu_baseline": {"value": value, "unit": "CSI estimates/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "CSI estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2206_05506_b200 as P
+    from paper_2206_05506_b200 import _lib
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = dict(WORKLOAD)
+    F = args.frames
+    cfg = P.PilotConfig(m=w["m"], c=w["c"], n_t=w["n_t"], n_batch=w["n_batch"], l=w["l"], f_s=10e6)
+    corr = P.Correlator(P.default_spec(10), cfg, w["n_r"], dtype=args.dtype, device=dev)
+
+    # --- resident synthetic input: a pool of distinct frame-sets tiled to F (> L2)
+    pool_n = min(F, 64)
+    pool, _ = synth_iq_pool(corr, pool_n, w, seed=1234 + rank, dev=dev)
+    iq = torch.empty(corr.iq_shape(F), dtype=torch.float32, device=dev)
+    for s in range(0, F, pool_n):
+        e = min(F, s + pool_n)
+        iq[s:e].copy_(pool[:e - s])
+    del pool
+    taps = torch.empty(corr.taps_shape(F), dtype=torch.complex64, device=dev)
+    ws = corr.workspace(F)
+    packed = ws[:corr.workspace_bytes(F)].view(torch.float16 if args.dtype == "fp16" else torch.bfloat16)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        _lib.check(_lib.lib().pnce_pack_iq(corr._plan, iq.data_ptr(), packed.data_ptr(), F, stream.cuda_stream))
+        if evs is not None:
+            evs[1].record(stream)
+        _lib.check(_lib.lib().pnce_correlate(corr._plan, packed.data_ptr(), taps.data_ptr(), None, None, F,
+                                             stream.cuda_stream))
+        if evs is not None:
+            evs[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.25)
+    launches0 = _lib.lib().pnce_kernel_launches()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        step(evs[i])
+    torch.cuda.synchronize(dev)
+    launches = _lib.lib().pnce_kernel_launches() - launches0
+    clocks = sampler.stop()
+    t_total = sum(e[0].elapsed_time(e[2]) for e in evs) / 1e3            # s, device time
+    t_pack = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3 / args.steps
+    t_corr = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3 / args.steps
+    if world > 1:
+        t = torch.tensor([t_total, t_pack, t_corr], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total, t_pack, t_corr = (float(x) for x in t.tolist())
+    ms_per_step = t_total / args.steps * 1e3
+    frames_total = F * world
+    frames_per_s = frames_total * args.steps / t_total
+    value = frames_per_s * w["n_r"] * w["n_t"]
+
+    # --- roofline of the dominant kernel (k_correlate)
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
+    flop_f, bytes_gemm_f, bytes_pack_f = algorithmic_per_frame(w)
+    achieved_tf = flop_f * F / t_corr / 1e12
+    achieved_hbm = bytes_gemm_f * F / t_corr / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                traffic = json.load(fh).get("k_correlate_bytes_per_frame")
+                traffic = traffic * F if traffic else None
+        except Exception:
+            traffic = None
+
+    # --- e2e through the public API with pinned host buffers (H2D in, D2H taps out)
+    e2e = None
+    if not args.no_e2e:
+        Fe = min(args.e2e_frames, F)
+        host_iq = torch.empty(corr.iq_shape(Fe), dtype=torch.float32).pin_memory()
+        host_iq.copy_(iq[:Fe].cpu())
+        host_taps = torch.empty(corr.taps_shape(Fe), dtype=torch.complex64).pin_memory()
+        for _ in range(2):
+            corr.process_host(host_iq, host_taps)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        reps = max(2, args.steps // 2)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(reps):
+            corr.process_host(host_iq, host_taps)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        te = t0.elapsed_time(t1) / 1e3
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": Fe * world * reps / te * w["n_r"] * w["n_t"], "unit": "CSI estimates/s",
+               "h2d_bytes_per_step": host_iq.numel() * 4, "d2h_bytes_per_step": host_taps.numel() * 8,
+               "frames_per_step": Fe, "us_per_frame": te / (Fe * reps) * 1e6}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, cores, sample, _ = cpu_reference_rate(w, seconds=args.cpu_seconds)
+        cpu = {"value": rate, "unit": "CSI estimates/s", "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "CSI estimates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "us_per_frame": ms_per_step * 1e3 / F, "frames_per_s": frames_per_s,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic (device-generated, draw_channel law, 10 dB AWGN)",
+            "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8 (BASELINE configs[2])",
+                       "frames_per_step": F, "input_bytes_per_step": iq.numel() * 4,
+                       "l2": "inputs (47 GB f32 IQ at 10k frames) >> 126 MB L2; no flush needed",
+                       "parallelism": f"dp{world} (frames sharded, no hot-path collective)"},
+            "tensor_pct_of_peak": 100 * achieved_tf / tf_burst,
+            "kernels": {"k_pack_iq_ms": t_pack * 1e3, "k_correlate_ms": t_corr * 1e3,
+                        "k_correlate_tflops": achieved_tf, "k_correlate_gbs": achieved_hbm,
+                        "k_pack_gbs": bytes_pack_f * F / t_pack / 1e9},
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": tf_burst, "unit": "TFLOP/s",
+                         "frac": achieved_tf / tf_burst, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 dense burst",
+                         "frac_of_sustained": achieved_tf / tf_sust if tf_sust else None,
+                         "hbm_frac": achieved_hbm / hbm,
+                         "algorithmic": {"flop_per_frame": flop_f, "bytes_per_frame": bytes_gemm_f,
+                                         "frames_per_launch": F}},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=10000, help="frame-sets per step per GPU")
+    ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--e2e-frames", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    try:
+        return run_gpu(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

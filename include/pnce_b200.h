@@ -1,0 +1,125 @@
+/*
+ * pnce_b200 — C ABI of the B200-native PN-correlation channel estimator.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   process_frames -> correlate_rows        (pnce/experiments.py:176-208,
+ *                                            pnce/estimator.py:68-86)
+ * Plain pointers and sizes only; no torch types.  All device pointers are
+ * caller-owned CUDA allocations; `stream` is a cudaStream_t passed as void*.
+ * Every entry point is reentrant (no hidden global state beyond a
+ * thread-local error string) and returns a pnce_status_t; on failure
+ * pnce_last_error() describes the failure on the calling thread.
+ *
+ * Layouts (row-major, little-endian):
+ *   iq     float32 [n_frames][n_batches][n_r][P + L - 1][2]   (I, Q)
+ *          = the reference IQ file payload layout (pnce/iqfile.py:9-11),
+ *          one frame-set = all n_batches = ceil(n_t / n_batch) received batches.
+ *   taps   float32 [n_frames][n_r][n_t][L][2]  (complex64, CirEstimate.taps,
+ *          pnce/estimator.py:27-37, already normalised by 1/M).
+ *   truth  same layout as taps (ChannelRealization.taps, pnce/channel.py:79-88).
+ *   stats  float64 [n_frames][4] accumulated (+=):
+ *          {sum |h_est - h|, sum |h_est - h|^2, non-finite tap count, 0}.
+ */
+#ifndef PNCE_B200_H
+#define PNCE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes; each maps to the reference exception class named
+ * (pnce/errors.py:4-69) by the Python front end. */
+typedef enum pnce_status {
+    PNCE_OK = 0,
+    PNCE_ERR_INVALID_CONFIG = 1,    /* InvalidConfigError      errors.py:29  */
+    PNCE_ERR_INVALID_SPEC = 2,      /* InvalidSpecError        errors.py:25  */
+    PNCE_ERR_ZERO_STATE = 3,        /* ZeroStateError          errors.py:17  */
+    PNCE_ERR_NOT_MAXIMAL = 4,       /* NotMaximalLengthError   errors.py:21  */
+    PNCE_ERR_DIMENSION = 5,         /* DimensionMismatchError  errors.py:45  */
+    PNCE_ERR_FRAME_TOO_SHORT = 6,   /* FrameTooShortError      errors.py:49  */
+    PNCE_ERR_PLAN_MISMATCH = 7,     /* PlanMismatchError       errors.py:53  */
+    PNCE_ERR_ROWS_OUT_OF_RANGE = 8, /* RowsOutOfRangeError     errors.py:41  */
+    PNCE_ERR_SATURATION = 9,        /* SaturationDetectedError errors.py:57  */
+    PNCE_ERR_CUDA = 10,             /* CUDA runtime/driver failure            */
+    PNCE_ERR_UNSUPPORTED_DEVICE = 11/* not an sm_100 device                  */
+} pnce_status_t;
+
+/* Operand precision of the tensor-core contraction (fp32 accumulate). */
+enum { PNCE_DTYPE_FP16 = 0, PNCE_DTYPE_BF16 = 1 };
+
+/* PilotConfig (pnce/pilots.py:14-47) + receive array size + LfsrSpec
+ * (pnce/pn.py:39-71).  tap_mask bit (t-1) set <=> feedback tap t. */
+typedef struct pnce_cfg {
+    int32_t m;          /* PN length M = 2^degree - 1          */
+    int32_t c;          /* cyclic-prefix length C              */
+    int32_t n_t;        /* transmit antennas                   */
+    int32_t n_r;        /* receive antennas                    */
+    int32_t n_batch;    /* transmitters multiplexed per batch  */
+    int32_t l;          /* CIR length L                        */
+    int32_t degree;     /* LFSR degree k                       */
+    uint32_t tap_mask;  /* LFSR feedback taps                  */
+    uint32_t state;     /* LFSR start state (nonzero)          */
+    int32_t dtype;      /* PNCE_DTYPE_*                        */
+} pnce_cfg_t;
+
+typedef struct pnce_plan pnce_plan_t;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t pnce_version(void);
+
+/* Thread-local description of the last failure on this thread. */
+const char* pnce_last_error(void);
+
+/* Validate a configuration (PilotConfig.__post_init__ pilots.py:30-41,
+ * LfsrSpec.__post_init__ pn.py:53-67, build_batch_plan's separation
+ * check pilots.py:134-142).  Host only, no device work. */
+pnce_status_t pnce_config_check(const pnce_cfg_t* cfg);
+
+/* generate_mseq (pn.py:109-138) on the device: one LFSR period written as
+ * chips (+1.0f / -1.0f) to chips_dev[0..m).  Synchronises `stream` to run the
+ * period check; returns PNCE_ERR_NOT_MAXIMAL when the period is not 2^k-1. */
+pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state,
+                                 float* chips_dev, int32_t m, void* stream);
+
+/* Build the correlator state for a configuration (correlator_rows_for_plan,
+ * experiments.py:157-173): runs the device LFSR and builds the stacked
+ * lag-window circulant rows (batched_lag_rows, estimator.py:114-117) in
+ * tensor-core operand layout.  One-time; synchronises `stream`. */
+pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** plan, void* stream);
+pnce_status_t pnce_plan_destroy(pnce_plan_t* plan);
+
+/* Copy the plan's device-generated chips (float32 [m]) into dst_dev. */
+pnce_status_t pnce_plan_chips(const pnce_plan_t* plan, float* dst_dev, void* stream);
+
+/* Bytes of device workspace pnce_process_frames needs for n_frames. */
+size_t pnce_workspace_bytes(const pnce_plan_t* plan, int64_t n_frames);
+
+/* K2 alone: CP removal (remove_cp, estimator.py:40-47) + de-interleave +
+ * fp16/bf16 quantisation of received IQ into the contraction operand. */
+pnce_status_t pnce_pack_iq(const pnce_plan_t* plan, const float* iq, void* packed,
+                           int64_t n_frames, void* stream);
+
+/* K3+K4 alone: tensor-core correlation of packed samples with the PN
+ * circulant, fused 1/M normalisation, per-transmitter window demux into taps
+ * and (when truth != NULL) per-frame error statistics into stats. */
+pnce_status_t pnce_correlate(const pnce_plan_t* plan, const void* packed, float* taps,
+                             const float* truth, double* stats, int64_t n_frames,
+                             void* stream);
+
+/* Frame-set seam = process_frames (experiments.py:176-208) for n_frames
+ * frame-sets: pack + correlate + demux (+ scoring when truth != NULL). */
+pnce_status_t pnce_process_frames(const pnce_plan_t* plan, const float* iq, float* taps,
+                                  const float* truth, double* stats, void* workspace,
+                                  size_t workspace_bytes, int64_t n_frames, void* stream);
+
+/* Launch-count accounting: number of device kernels this library has
+ * launched in the calling process (for bench.py's gpu_launches). */
+int64_t pnce_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PNCE_B200_H */

@@ -1,0 +1,16 @@
+"""B200-native PN-correlation channel estimation (arXiv 2206.05506 hot path).
+
+Front end mirroring the reference package `pnce` for the estimation path;
+compute runs in libpnce_b200.so (sm_100a tcgen05/TMA kernels) via a C ABI.
+"""
+
+from .errors import *  # noqa: F401,F403
+from .estimator import (CirEstimate, Correlator, WorkCounters, correlator_rows_for_plan,  # noqa: F401
+                        process_frames, remove_cp)
+from .metrics import mae, mse  # noqa: F401
+from .pilots import (BatchAssignment, BatchPlan, PilotConfig, build_batch_plan,  # noqa: F401
+                     cyclic_separation, max_batch, propagation_time, shift_for_transmitter)
+from .pn import (PRIMITIVE_TAPS, LfsrSpec, PnSequence, default_spec, generate_mseq,  # noqa: F401
+                 sequence_for_length)
+
+__version__ = "0.1.0"

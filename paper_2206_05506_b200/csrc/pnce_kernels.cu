@@ -1,0 +1,656 @@
+// B200-native PN-correlation channel estimator: device kernels + C ABI.
+//
+// Hot path (reference: pnce/experiments.py:176-208 process_frames ->
+// pnce/estimator.py:68-86 correlate_rows):
+//   K1  k_lfsr / k_build_circulant : generate_mseq (pn.py:109-138) on device and
+//       the stacked lag-window rows A[j*L+l, k] = chip[(k - s_j - l) mod M]
+//       (estimator.py:62-65,114-117) as an fp16/bf16 K-major operand.
+//   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the
+//       received f32 (I,Q) samples into rows (frame, batch, rx, re|im) x K.
+//   K3  k_correlate : tcgen05 UMMA  D^T[rows, R] = B^T[rows, K] . A^T[K, R]
+//       (both real GEMMs of estimator.py:77-80 in one contraction; the huge
+//       frame x rx x re/im axis is the UMMA M dimension), TMA-fed, warp-specialised,
+//       persistent, TMEM double-buffered accumulator.
+//   K4  (fused into K3's epilogue) x 1/M, Re/Im pairing, per-transmitter window
+//       demux into taps[f, r, t, l] (experiments.py:206-207) and optional
+//       sum|e|, sum|e|^2, non-finite count vs. truth (metrics.py:19-25 + MSE).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <type_traits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pnce_b200.h"
+#include "sm100_ptx.cuh"
+
+using namespace pnce;
+
+namespace {
+
+constexpr int kBM = 128;       // UMMA M (input rows per tile)
+constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
+constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
+constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kSmemLimit = 227 * 1024;
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+pnce_status_t fail(pnce_status_t code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(PNCE_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ------------------------------------------------------------------ K1: LFSR
+// One thread runs the Fibonacci LFSR for one period (pn.py:115-137):
+// out = MSB, fb = parity(state & tap_mask), state = ((state << 1) | fb) & mask.
+__global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m,
+                       int* period_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t mask = (1u << degree) - 1u;
+    uint32_t s = state0;
+    int n = 0;
+    const int limit = 1 << degree;
+    for (int i = 0; i < limit; ++i) {
+        uint32_t bit = (s >> (degree - 1)) & 1u;
+        if (n < m) chips[n] = bit ? -1.0f : 1.0f;
+        ++n;
+        uint32_t fb = __popc(s & tap_mask) & 1u;
+        s = ((s << 1) | fb) & mask;
+        if (s == state0) break;
+    }
+    *period_out = n;
+}
+
+// Stacked lag-window rows, K-major, zero padded: A[n, k] for n < rows_alloc, k < k_pad.
+template <typename T>
+__global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m,
+                                  int k_pad, int r_total, int rows_alloc, int l, int spacing) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)rows_alloc * k_pad;
+    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        int n = (int)(idx / k_pad);
+        int k = (int)(idx % k_pad);
+        float v = 0.0f;
+        if (n < r_total && k < m) {
+            int lag = (spacing * (n / l) + (n % l)) % m;  // shift_for_transmitter + window lag
+            int ci = k - lag;
+            if (ci < 0) ci += m;
+            v = chips[ci];
+        }
+        if constexpr (sizeof(T) == 2 && std::is_same<T, __half>::value)
+            a[idx] = __float2half_rn(v);
+        else
+            a[idx] = __float2bfloat16_rn(v);
+    }
+}
+
+// ------------------------------------------------------------------ K2: pack
+// One thread per (link row q, 8-sample chunk c): read samples [C+8c, C+8c+8) of
+// row q (q = (f*nb + b)*n_r + r), write 8 quantised Re to packed row 2q and
+// 8 Im to row 2q+1 (16 B each); zero beyond M.
+template <typename T>
+__global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links,
+                          int samples, int c, int m, int k_pad) {
+    const int chunks = k_pad >> 3;
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t total = n_links * chunks;
+    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = idx / chunks;
+        const int ch = (int)(idx - q * chunks);
+        const int k0 = ch << 3;
+        const float2* src = reinterpret_cast<const float2*>(iq) + q * samples + c + k0;
+        float re[8], im[8];
+        if (k0 + 8 <= m) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float2 v = __ldg(src + j);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+        }
+        uint4 pr, pi;
+        T* hr = reinterpret_cast<T*>(&pr);
+        T* hi = reinterpret_cast<T*>(&pi);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if constexpr (std::is_same<T, __half>::value) {
+                hr[j] = __float2half_rn(re[j]);
+                hi[j] = __float2half_rn(im[j]);
+            } else {
+                hr[j] = __float2bfloat16_rn(re[j]);
+                hi[j] = __float2bfloat16_rn(im[j]);
+            }
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0);
+        dst[0] = pr;
+        *reinterpret_cast<uint4*>(out + (2 * q + 1) * (int64_t)k_pad + k0) = pi;
+    }
+}
+
+// ------------------------------------------------------------------ K3+K4
+struct CorrParams {
+    int64_t total_rows;  // n_frames * n_batches * n_r * 2
+    int32_t m_tiles;
+    int32_t n_tiles;
+    int32_t bn;
+    int32_t k_blocks;
+    int32_t stages;
+    uint32_t stage_bytes;
+    uint32_t idesc;
+    uint32_t tmem_cols;
+    int32_t n_r, n_t, n_batches, n_batch, l;
+    float inv_m;
+    float* taps;
+    const float* truth;
+    double* stats;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
+            const CorrParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const int S = p.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_in);
+        tma_prefetch(&tm_circ);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int total_tiles = p.m_tiles * p.n_tiles;
+    const uint32_t a_bytes = kBM * kBK * 2;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer
+            const uint64_t pol_in = policy_evict_first();
+            const uint64_t pol_circ = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+                const int mt = tile / p.n_tiles;
+                const int nt = tile - mt * p.n_tiles;
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+                    uint8_t* sb = sa + a_bytes;
+                    mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
+                    tma_load_2d(sa, &tm_in, &full[stage], kb * kBK, mt * kBM, pol_in);
+                    tma_load_2d(sb, &tm_circ, &full[stage], kb * kBK, nt * p.bn, pol_circ);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer (single thread)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                    const uint32_t sb = sa + a_bytes;
+#pragma unroll
+                    for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
+                        const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
+                        const uint64_t bd = make_sdesc(sb + ks * 32, 16, 1024, 2);
+                        umma_f16_ss(d_tmem, ad, bd, p.idesc, (kb | ks) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4
+        const int quarter = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            const int mt = tile / p.n_tiles;
+            const int nt = tile - mt * p.n_tiles;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+
+            const int64_t row = (int64_t)mt * kBM + quarter * 32 + lane;
+            const bool row_ok = row < p.total_rows;
+            const bool odd = (lane & 1) != 0;
+            const int64_t link = row >> 1;
+            const int r = (int)(link % p.n_r);
+            const int64_t fb = link / p.n_r;
+            const int b = (int)(fb % p.n_batches);
+            const int64_t f = fb / p.n_batches;
+            const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
+            const int n_valid = n_tx * p.l;
+            const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
+            float2* taps = reinterpret_cast<float2*>(p.taps);
+            const float2* truth = reinterpret_cast<const float2*>(p.truth);
+            float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
+
+            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.bn);
+            for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                float v[16];
+                tmem_ld16(t_row + c0, v);
+                float x[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float send = odd ? v[i] : v[8 + i];
+                    x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
+                }
+                const int n_first = nt * p.bn + c0 + (odd ? 8 : 0);
+                if (row_ok) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int n = n_first + i;
+                        if (n < n_valid) {
+                            float2 e;
+                            e.x = (odd ? x[i] : v[i]) * p.inv_m;
+                            e.y = (odd ? v[8 + i] : x[i]) * p.inv_m;
+                            taps[out_base + n] = e;
+                            if (!isfinite(e.x) || !isfinite(e.y)) s_bad += 1.f;
+                            if (truth != nullptr) {
+                                const float2 h = __ldg(truth + out_base + n);
+                                const float dx = e.x - h.x, dy = e.y - h.y;
+                                const float sq = dx * dx + dy * dy;
+                                s_sq += sq;
+                                s_abs += sqrtf(sq);
+                            }
+                        }
+                    }
+                }
+            }
+            // TMEM stage fully read -> release it to the MMA warp.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+
+            if (p.stats != nullptr) {
+                // per-frame reduction: warp-uniform frame -> one atomic per warp.
+                // Rows of a warp are contiguous, so lane 0 holds the first valid row.
+                const bool lead_ok = __shfl_sync(0xffffffffu, row_ok, 0);
+                const int64_t f0 = __shfl_sync(0xffffffffu, f, 0);
+                const bool uniform = __all_sync(0xffffffffu, (f == f0) || !row_ok);
+                if (uniform) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+                        s_sq += __shfl_xor_sync(0xffffffffu, s_sq, o);
+                        s_bad += __shfl_xor_sync(0xffffffffu, s_bad, o);
+                    }
+                    if (lane == 0 && lead_ok) {
+                        if (p.truth != nullptr) {
+                            atomicAdd(&p.stats[f0 * 4 + 0], (double)s_abs);
+                            atomicAdd(&p.stats[f0 * 4 + 1], (double)s_sq);
+                        }
+                        if (s_bad != 0.f) atomicAdd(&p.stats[f0 * 4 + 2], (double)s_bad);
+                    }
+                } else if (row_ok) {
+                    if (p.truth != nullptr) {
+                        atomicAdd(&p.stats[f * 4 + 0], (double)s_abs);
+                        atomicAdd(&p.stats[f * 4 + 1], (double)s_sq);
+                    }
+                    if (s_bad != 0.f) atomicAdd(&p.stats[f * 4 + 2], (double)s_bad);
+                }
+            }
+        }
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, p.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128B swizzle.
+pnce_status_t make_tmap(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                        uint32_t box_rows, int bf16) {
+    auto enc = get_encode();
+    if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return PNCE_OK;
+}
+
+}  // namespace
+
+struct pnce_plan {
+    pnce_cfg_t cfg;
+    int n_batches;
+    int r_total;     // N_b * L
+    int k_pad;       // roundup(M, 64)
+    int bn;          // UMMA N per tile
+    int n_tiles;     // ceil(R / bn)
+    int rows_alloc;  // n_tiles * bn
+    int stages;
+    uint32_t stage_bytes;
+    uint32_t tmem_cols;
+    int num_sms;
+    float* chips;    // device [m]
+    void* circ;      // device [rows_alloc][k_pad] 16-bit
+    CUtensorMap tm_circ;
+};
+
+extern "C" {
+
+int32_t pnce_version(void) { return 100; }
+
+const char* pnce_last_error(void) { return g_err.c_str(); }
+
+int64_t pnce_kernel_launches(void) { return g_launches.load(); }
+
+pnce_status_t pnce_config_check(const pnce_cfg_t* cfg) {
+    if (!cfg) return fail(PNCE_ERR_INVALID_CONFIG, "null config");
+    if (cfg->degree < 2 || cfg->degree > 16)
+        return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
+    const uint32_t full = (1u << cfg->degree) - 1u;
+    if (cfg->state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
+    if (cfg->state > full) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
+    if (!(cfg->tap_mask & (1u << (cfg->degree - 1))))
+        return fail(PNCE_ERR_INVALID_SPEC, "tap set must include the degree");
+    if (cfg->tap_mask & ~full) return fail(PNCE_ERR_INVALID_SPEC, "tap outside [1, degree]");
+    if ((int64_t)cfg->m != (int64_t)full)
+        return fail(PNCE_ERR_INVALID_CONFIG, "m must equal 2^degree - 1");
+    if (cfg->n_t < 1 || cfg->n_r < 1) return fail(PNCE_ERR_INVALID_CONFIG, "n_t, n_r must be >= 1");
+    if (!(1 <= cfg->l && cfg->l <= cfg->c && cfg->c <= cfg->m))
+        return fail(PNCE_ERR_INVALID_CONFIG, "need 1 <= L <= C <= M");
+    if (!(1 <= cfg->n_batch && cfg->n_batch <= cfg->m / cfg->c))
+        return fail(PNCE_ERR_INVALID_CONFIG, "n_batch outside [1, floor(M/C)]");
+    if (cfg->dtype != PNCE_DTYPE_FP16 && cfg->dtype != PNCE_DTYPE_BF16)
+        return fail(PNCE_ERR_INVALID_CONFIG, "dtype must be fp16 or bf16");
+    // build_batch_plan separation check (pilots.py:134-142)
+    const int spacing = cfg->m / cfg->n_batch;
+    for (int i = 0; i < cfg->n_batch; ++i)
+        for (int j = i + 1; j < cfg->n_batch; ++j) {
+            int d = (spacing * (j - i)) % cfg->m;
+            d = d < cfg->m - d ? d : cfg->m - d;
+            if (d < cfg->l) return fail(PNCE_ERR_INVALID_CONFIG, "shift separation < L");
+        }
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state, float* chips_dev,
+                                 int32_t m, void* stream) {
+    if (degree < 2 || degree > 16) return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
+    if (state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
+    if (state >= (1u << degree)) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
+    if (m != (int32_t)((1u << degree) - 1u)) return fail(PNCE_ERR_DIMENSION, "m must be 2^degree - 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int* d_period = nullptr;
+    CUDA_TRY(cudaMallocAsync(&d_period, sizeof(int), st));
+    k_lfsr<<<1, 1, 0, st>>>(degree, tap_mask, state, chips_dev, m, d_period);
+    g_launches++;
+    int period = 0;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&period, d_period, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(d_period, st);
+    if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("k_lfsr: ") + cudaGetErrorString(e));
+    if (period != m)
+        return fail(PNCE_ERR_NOT_MAXIMAL, "LFSR period " + std::to_string(period) + " != " +
+                                              std::to_string(m) + "; feedback polynomial is not primitive");
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* stream) {
+    if (!out) return fail(PNCE_ERR_INVALID_CONFIG, "null plan out-pointer");
+    *out = nullptr;
+    pnce_status_t s = pnce_config_check(cfg);
+    if (s != PNCE_OK) return s;
+    int dev = 0, major = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return fail(PNCE_ERR_UNSUPPORTED_DEVICE, "pnce_b200 needs an sm_100 (B200) device");
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+
+    pnce_plan* p = new pnce_plan();
+    p->cfg = *cfg;
+    p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
+    p->r_total = cfg->n_batch * cfg->l;
+    p->k_pad = (cfg->m + kBK - 1) / kBK * kBK;
+    // UMMA N per tile: multiple of 16 in [16, 256]; balance tiles.
+    const int r16 = (p->r_total + 15) / 16 * 16;
+    p->n_tiles = (r16 + 255) / 256;
+    p->bn = ((r16 + p->n_tiles - 1) / p->n_tiles + 15) / 16 * 16;
+    p->rows_alloc = p->n_tiles * p->bn;
+    p->stage_bytes = (uint32_t)(kBM * kBK * 2 + p->bn * kBK * 2);
+    const size_t barrier_bytes = 1024;
+    int stages = (int)((kSmemLimit - 1024 - barrier_bytes) / p->stage_bytes);
+    p->stages = stages > 8 ? 8 : stages;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * p->bn)) cols <<= 1;
+    p->tmem_cols = cols;
+    p->num_sms = sms;
+
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
+    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
+    if (e != cudaSuccess) {
+        pnce_plan_destroy(p);
+        return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
+    }
+    s = pnce_generate_mseq(cfg->degree, cfg->tap_mask, cfg->state, p->chips, cfg->m, stream);
+    if (s != PNCE_OK) {
+        pnce_plan_destroy(p);
+        return s;
+    }
+    const int spacing = cfg->m / cfg->n_batch;
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    if (cfg->dtype == PNCE_DTYPE_BF16)
+        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
+    else
+        k_build_circulant<__half><<<blocks, 256, 0, st>>>(
+            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
+    g_launches++;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        pnce_plan_destroy(p);
+        return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
+    }
+    s = make_tmap(&p->tm_circ, p->circ, p->k_pad, p->rows_alloc, p->bn, cfg->dtype == PNCE_DTYPE_BF16);
+    if (s != PNCE_OK) {
+        pnce_plan_destroy(p);
+        return s;
+    }
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_err = cudaFuncSetAttribute(k_correlate, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    });
+    if (attr_err != cudaSuccess) {
+        pnce_plan_destroy(p);
+        return fail(PNCE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    }
+    *out = p;
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
+    if (!p) return PNCE_OK;
+    if (p->chips) cudaFree(p->chips);
+    if (p->circ) cudaFree(p->circ);
+    delete p;
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_plan_chips(const pnce_plan_t* p, float* dst, void* stream) {
+    if (!p || !dst) return fail(PNCE_ERR_INVALID_CONFIG, "null plan or destination");
+    CUDA_TRY(cudaMemcpyAsync(dst, p->chips, sizeof(float) * p->cfg.m, cudaMemcpyDeviceToDevice,
+                             static_cast<cudaStream_t>(stream)));
+    return PNCE_OK;
+}
+
+size_t pnce_workspace_bytes(const pnce_plan_t* p, int64_t n_frames) {
+    if (!p || n_frames < 0) return 0;
+    const int64_t rows = n_frames * p->n_batches * (int64_t)p->cfg.n_r * 2;
+    return (size_t)rows * p->k_pad * 2;
+}
+
+pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, int64_t n_frames,
+                           void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
+    if (n_frames == 0) return PNCE_OK;
+    if (!iq || !packed) return fail(PNCE_ERR_DIMENSION, "null buffer");
+    if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
+    const pnce_cfg_t& c = p->cfg;
+    const int samples = c.c + c.m + c.l - 1;
+    const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
+    const int64_t work = links * (p->k_pad / 8);
+    const int64_t want = (work + 255) / 256;
+    const int blocks = (int)(want < (int64_t)p->num_sms * 16 ? want : (int64_t)p->num_sms * 16);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (c.dtype == PNCE_DTYPE_BF16)
+        k_pack_iq<__nv_bfloat16><<<blocks, 256, 0, st>>>(iq, (__nv_bfloat16*)packed, links, samples, c.c, c.m, p->k_pad);
+    else
+        k_pack_iq<__half><<<blocks, 256, 0, st>>>(iq, (__half*)packed, links, samples, c.c, c.m, p->k_pad);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
+                             double* stats, int64_t n_frames, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
+    if (n_frames == 0) return PNCE_OK;
+    if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
+    if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(taps) & 7) || (truth && (reinterpret_cast<uintptr_t>(truth) & 7)))
+        return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
+    const pnce_cfg_t& c = p->cfg;
+    CorrParams prm{};
+    prm.total_rows = n_frames * p->n_batches * (int64_t)c.n_r * 2;
+    const int64_t m_tiles = (prm.total_rows + kBM - 1) / kBM;
+    if (m_tiles * p->n_tiles > INT32_MAX) return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
+    if (prm.total_rows > INT32_MAX) return fail(PNCE_ERR_DIMENSION, "too many rows for one tensor map");
+    prm.m_tiles = (int32_t)m_tiles;
+    prm.n_tiles = p->n_tiles;
+    prm.bn = p->bn;
+    prm.k_blocks = p->k_pad / kBK;
+    prm.stages = p->stages;
+    prm.stage_bytes = p->stage_bytes;
+    prm.idesc = make_idesc_f16(kBM, p->bn, c.dtype == PNCE_DTYPE_BF16);
+    prm.tmem_cols = p->tmem_cols;
+    prm.n_r = c.n_r;
+    prm.n_t = c.n_t;
+    prm.n_batches = p->n_batches;
+    prm.n_batch = c.n_batch;
+    prm.l = c.l;
+    prm.inv_m = 1.0f / (float)c.m;
+    prm.taps = taps;
+    prm.truth = truth;
+    prm.stats = stats;
+    CUtensorMap tm_in;
+    pnce_status_t s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, c.dtype == PNCE_DTYPE_BF16);
+    if (s != PNCE_OK) return s;
+    const int64_t tiles = m_tiles * p->n_tiles;
+    const int grid = (int)(tiles < p->num_sms ? tiles : p->num_sms);
+    const size_t smem = 1024 + (size_t)p->stages * p->stage_bytes + 256;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_correlate<<<grid, kThreads, smem, st>>>(tm_in, p->tm_circ, prm);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                  double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
+                                  void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames == 0) return PNCE_OK;
+    if (workspace_bytes < pnce_workspace_bytes(p, n_frames))
+        return fail(PNCE_ERR_DIMENSION, "workspace too small");
+    pnce_status_t s = pnce_pack_iq(p, iq, workspace, n_frames, stream);
+    if (s != PNCE_OK) return s;
+    return pnce_correlate(p, workspace, taps, truth, stats, n_frames, stream);
+}
+
+}  // extern "C"
