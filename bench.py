@@ -1,7 +1,8 @@
 """Benchmark: PN-correlation channel estimation at 64x64 MIMO, PN 1023 (BASELINE cfg3).
 
-One step = one pass of the hot path (pack -> tcgen05 correlate -> fused 1/M + demux)
-over a batch of F frame-sets already resident in HBM (default F = 10,000, the
+One step = one pass of the hot path over a batch of F frame-sets already resident in
+HBM: ONE fused kernel launch (CP strip + fp16 quantise + tcgen05 correlation with the
+PN circulant + 1/M + per-transmitter demux into complex64 taps) (default F = 10,000, the
 BASELINE headline: 47 GB of received IQ, far larger than L2).  value = CSI
 estimates/s = link CIRs (frame, rx, tx) per second over all ranks.
 
@@ -42,14 +43,16 @@ def load_peaks():
 
 
 def algorithmic_per_frame(w):
-    """FLOP = 4*macs (macs = n_t*L*M*n_r), bytes = fp16 body in + c64 taps out."""
+    """FLOP = 4*macs (macs = n_t*L*M*n_r, experiments.py:200).
+    bytes_gemm  = fp16 body in + complex64 taps out (packed-operand GEMM, §8d);
+    bytes_fused = f32 (I,Q) CP-stripped body in + complex64 taps out (the fused kernel)."""
     n_batches = -(-w["n_t"] // w["n_batch"])
     macs = w["n_t"] * w["l"] * w["m"] * w["n_r"]
     flop = 4 * macs
-    bytes_gemm = w["n_r"] * n_batches * w["m"] * 2 * 2 + w["n_r"] * w["n_t"] * w["l"] * 8
-    samples = w["c"] + w["m"] + w["l"] - 1
-    bytes_pack = w["n_r"] * n_batches * samples * 8 + w["n_r"] * n_batches * 2 * (-(-w["m"] // 64) * 64) * 2
-    return flop, bytes_gemm, bytes_pack
+    taps = w["n_r"] * w["n_t"] * w["l"] * 8
+    bytes_gemm = w["n_r"] * n_batches * w["m"] * 2 * 2 + taps
+    bytes_fused = w["n_r"] * n_batches * w["m"] * 8 + taps
+    return flop, bytes_gemm, bytes_fused
 
 
 class ClockSampler:
@@ -227,20 +230,13 @@ def run_gpu(args, rank, world):
         iq[s:e].copy_(pool[:e - s])
     del pool
     taps = torch.empty(corr.taps_shape(F), dtype=torch.complex64, device=dev)
-    ws = corr.workspace(F)
-    packed = ws[:corr.workspace_bytes(F)].view(torch.float16 if args.dtype == "fp16" else torch.bfloat16)
     stream = torch.cuda.current_stream(dev)
+    L = _lib.lib()
 
-    def step(evs=None):
-        if evs is not None:
-            evs[0].record(stream)
-        _lib.check(_lib.lib().pnce_pack_iq(corr._plan, iq.data_ptr(), packed.data_ptr(), F, stream.cuda_stream))
-        if evs is not None:
-            evs[1].record(stream)
-        _lib.check(_lib.lib().pnce_correlate(corr._plan, packed.data_ptr(), taps.data_ptr(), None, None, F,
-                                             stream.cuda_stream))
-        if evs is not None:
-            evs[2].record(stream)
+    def step():
+        # the hot path: ONE fused launch (CP strip + quantise + tcgen05 correlate + demux + 1/M)
+        _lib.check(L.pnce_process_frames(corr._plan, iq.data_ptr(), taps.data_ptr(), None, None, None, 0, F,
+                                         stream.cuda_stream))
 
     for _ in range(args.warmup):
         step()
@@ -250,40 +246,66 @@ def run_gpu(args, rank, world):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.25)
-    launches0 = _lib.lib().pnce_kernel_launches()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = L.pnce_kernel_launches()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     torch.cuda.synchronize(dev)
+    evs[0].record(stream)
     for i in range(args.steps):
-        step(evs[i])
+        step()
+        evs[i + 1].record(stream)
     torch.cuda.synchronize(dev)
-    launches = _lib.lib().pnce_kernel_launches() - launches0
+    launches = L.pnce_kernel_launches() - launches0
     clocks = sampler.stop()
-    t_total = sum(e[0].elapsed_time(e[2]) for e in evs) / 1e3            # s, device time
-    t_pack = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3 / args.steps
-    t_corr = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3 / args.steps
+    t_total = evs[0].elapsed_time(evs[-1]) / 1e3                      # s, device time
+    t_step = [evs[i].elapsed_time(evs[i + 1]) / 1e3 for i in range(args.steps)]
+    t_kernel = sum(t_step) / args.steps                                # one launch per step
     if world > 1:
-        t = torch.tensor([t_total, t_pack, t_corr], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_total, t_kernel], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total, t_pack, t_corr = (float(x) for x in t.tolist())
+        t_total, t_kernel = (float(x) for x in t.tolist())
     ms_per_step = t_total / args.steps * 1e3
     frames_total = F * world
     frames_per_s = frames_total * args.steps / t_total
     value = frames_per_s * w["n_r"] * w["n_t"]
 
-    # --- roofline of the dominant kernel (k_correlate)
+    # --- roofline of the dominant (only) kernel: fused k_correlate<true>
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
-    flop_f, bytes_gemm_f, bytes_pack_f = algorithmic_per_frame(w)
-    achieved_tf = flop_f * F / t_corr / 1e12
-    achieved_hbm = bytes_gemm_f * F / t_corr / 1e9
+    flop_f, bytes_gemm_f, bytes_fused_f = algorithmic_per_frame(w)
+    achieved_tf = flop_f * F / t_kernel / 1e12
+    achieved_gbs = bytes_fused_f * F / t_kernel / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as fh:
-                traffic = json.load(fh).get("k_correlate_bytes_per_frame")
-                traffic = traffic * F if traffic else None
+                per_frame = json.load(fh).get("k_correlate_fused_dram_bytes_per_frame")
+                traffic = per_frame * F if per_frame else None
         except Exception:
             traffic = None
+
+    # --- GEMM-only leg (K3 on the pre-packed fp16 operand): the north-star tensor-% number
+    gemm = None
+    if not args.no_gemm_leg:
+        Fg = min(F, args.gemm_frames)
+        packed = corr.pack(iq[:Fg])
+        taps_g = taps[:Fg]
+        for _ in range(3):
+            _lib.check(L.pnce_correlate(corr._plan, packed.data_ptr(), taps_g.data_ptr(), None, None, Fg,
+                                        stream.cuda_stream))
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        g0.record(stream)
+        for _ in range(args.steps):
+            _lib.check(L.pnce_correlate(corr._plan, packed.data_ptr(), taps_g.data_ptr(), None, None, Fg,
+                                        stream.cuda_stream))
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        tg = g0.elapsed_time(g1) / 1e3 / args.steps
+        gemm = {"kernel": "k_correlate<packed>", "frames": Fg, "us_per_frame": tg / Fg * 1e6,
+                "tflops": flop_f * Fg / tg / 1e12, "frac_of_bf16_peak": flop_f * Fg / tg / 1e12 / tf_burst,
+                "gbs": bytes_gemm_f * Fg / tg / 1e9}
+        del packed
 
     # --- e2e through the public API with pinned host buffers (H2D in, D2H taps out)
     e2e = None
@@ -331,16 +353,15 @@ def run_gpu(args, rank, world):
                        "l2": "inputs (47 GB f32 IQ at 10k frames) >> 126 MB L2; no flush needed",
                        "parallelism": f"dp{world} (frames sharded, no hot-path collective)"},
             "tensor_pct_of_peak": 100 * achieved_tf / tf_burst,
-            "kernels": {"k_pack_iq_ms": t_pack * 1e3, "k_correlate_ms": t_corr * 1e3,
-                        "k_correlate_tflops": achieved_tf, "k_correlate_gbs": achieved_hbm,
-                        "k_pack_gbs": bytes_pack_f * F / t_pack / 1e9},
-            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": tf_burst, "unit": "TFLOP/s",
-                         "frac": achieved_tf / tf_burst, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 dense burst",
-                         "frac_of_sustained": achieved_tf / tf_sust if tf_sust else None,
-                         "hbm_frac": achieved_hbm / hbm,
-                         "algorithmic": {"flop_per_frame": flop_f, "bytes_per_frame": bytes_gemm_f,
+            "kernels": {"k_correlate_fused_ms": t_kernel * 1e3, "tflops": achieved_tf, "gbs": achieved_gbs},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm, "traffic": traffic,
+                         "peak_source": f"{peak_src} HBM copy bandwidth",
+                         "tensor_frac": achieved_tf / tf_burst,
+                         "algorithmic": {"flop_per_frame": flop_f, "bytes_per_frame": bytes_fused_f,
+                                         "bytes": "f32 CP-stripped body in + complex64 taps out",
                                          "frames_per_launch": F}},
+            "gemm_leg": gemm,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -358,6 +379,8 @@ def main():
     ap.add_argument("--e2e-frames", type=int, default=512)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gemm-leg", action="store_true")
+    ap.add_argument("--gemm-frames", type=int, default=4096)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -94,7 +94,7 @@ pnce_status_t pnce_plan_destroy(pnce_plan_t* plan);
 /* Copy the plan's device-generated chips (float32 [m]) into dst_dev. */
 pnce_status_t pnce_plan_chips(const pnce_plan_t* plan, float* dst_dev, void* stream);
 
-/* Bytes of device workspace pnce_process_frames needs for n_frames. */
+/* Bytes of the packed 16-bit operand pnce_pack_iq writes for n_frames. */
 size_t pnce_workspace_bytes(const pnce_plan_t* plan, int64_t n_frames);
 
 /* K2 alone: CP removal (remove_cp, estimator.py:40-47) + de-interleave +
@@ -110,7 +110,9 @@ pnce_status_t pnce_correlate(const pnce_plan_t* plan, const void* packed, float*
                              void* stream);
 
 /* Frame-set seam = process_frames (experiments.py:176-208) for n_frames
- * frame-sets: pack + correlate + demux (+ scoring when truth != NULL). */
+ * frame-sets in ONE fused kernel: CP strip + quantise (K2) inside the
+ * tcgen05 correlation (K3) + demux/normalise/scoring epilogue (K4).  No packed
+ * intermediate is written; `workspace` may be NULL (kept for ABI stability). */
 pnce_status_t pnce_process_frames(const pnce_plan_t* plan, const float* iq, float* taps,
                                   const float* truth, double* stats, void* workspace,
                                   size_t workspace_bytes, int64_t n_frames, void* stream);

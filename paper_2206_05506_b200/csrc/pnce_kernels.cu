@@ -151,6 +151,15 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
 }
 
 // ------------------------------------------------------------------ K3+K4
+// Correlation kernel.  FUSED=true reads the raw f32 (I,Q) frames directly: eight
+// converter warps perform remove_cp + de-interleave + fp16/bf16 quantisation
+// straight into the 128B-swizzled UMMA A stage (K2 fused away, no packed
+// intermediate in HBM).  FUSED=false consumes the packed operand through TMA.
+constexpr int kConvWarps = 8;
+constexpr int kFusedThreads = (6 + kConvWarps) * 32;
+constexpr int kLinksPerTile = kBM / 2;                                    // 64 (re, im) row pairs
+constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 2
+
 struct CorrParams {
     int64_t total_rows;  // n_frames * n_batches * n_r * 2
     int32_t m_tiles;
@@ -162,13 +171,147 @@ struct CorrParams {
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
+    int32_t m, c, samples;  // PN length, CP length, samples per received row (fused input)
+    int32_t bf16;
     float inv_m;
+    const float* iq;
     float* taps;
     const float* truth;
     double* stats;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+// One converter task: 8 consecutive body samples of one link -> 16 B of Re, 16 B of Im.
+struct ConvTask {
+    float re[8], im[8];
+};
+
+__device__ __forceinline__ void conv_load(const CorrParams& p, int mt, int kb, int task, ConvTask& t) {
+    const int link_local = task >> 3;
+    const int chunk = task & 7;
+    const int64_t q = (int64_t)mt * kLinksPerTile + link_local;
+    const int k0 = kb * kBK + chunk * 8;
+    const int64_t total_links = p.total_rows >> 1;
+    if (q < total_links && k0 + 8 <= p.m) {
+        const int64_t s0 = q * p.samples + p.c + k0;  // complex index
+        const float* src = p.iq + 2 * s0;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 v = __ldg(s4 + j);
+                t.re[2 * j] = v.x;
+                t.im[2 * j] = v.y;
+                t.re[2 * j + 1] = v.z;
+                t.im[2 * j + 1] = v.w;
+            }
+        } else {
+            const float2* s2 = reinterpret_cast<const float2*>(src);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float2 v = __ldg(s2 + j);
+                t.re[j] = v.x;
+                t.im[j] = v.y;
+            }
+        }
+    } else {
+        const bool ok = q < total_links;
+        const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float2 v = (ok && k0 + j < p.m) ? __ldg(s2 + j) : make_float2(0.f, 0.f);
+            t.re[j] = v.x;
+            t.im[j] = v.y;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
+    if (bf16) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void conv_store(uint8_t* stage_a, int task, const ConvTask& t, int bf16) {
+    const int link_local = task >> 3;
+    const int chunk = task & 7;
+    const int row_re = 2 * link_local;
+    const int row_im = row_re + 1;
+    uint4 vr, vi;
+    vr.x = pack2(t.re[0], t.re[1], bf16);
+    vr.y = pack2(t.re[2], t.re[3], bf16);
+    vr.z = pack2(t.re[4], t.re[5], bf16);
+    vr.w = pack2(t.re[6], t.re[7], bf16);
+    vi.x = pack2(t.im[0], t.im[1], bf16);
+    vi.y = pack2(t.im[2], t.im[3], bf16);
+    vi.z = pack2(t.im[4], t.im[5], bf16);
+    vi.w = pack2(t.im[6], t.im[7], bf16);
+    // 128B swizzle: 16-byte chunk c of row r lives at chunk position c ^ (r % 8)
+    *reinterpret_cast<uint4*>(stage_a + row_re * 128 + ((chunk ^ (row_re & 7)) << 4)) = vr;
+    *reinterpret_cast<uint4*>(stage_a + row_im * 128 + ((chunk ^ (row_im & 7)) << 4)) = vi;
+}
+
+// Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
+__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok,
+                                          int n_first, int n_valid, int64_t out_base, float& s_abs,
+                                          float& s_sq, float& s_bad) {
+    // Re/Im pairing: the even lane keeps columns 0..7, the odd lane columns 8..15.
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float send = __uint_as_float(odd ? v[i] : v[8 + i]);
+        x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    if (!row_ok) return;
+    float o[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
+        o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
+    const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
+    if (n_first + 8 <= n_valid && (g & 3) == 0) {
+        float* dst = p.taps + 2 * g;
+        st_global_v8(dst, *reinterpret_cast<const float(*)[8]>(&o[0]));
+        st_global_v8(dst + 8, *reinterpret_cast<const float(*)[8]>(&o[8]));
+        if (p.truth != nullptr) {
+            float h[16];
+            ld_global_nc_v8(p.truth + 2 * g, *reinterpret_cast<float(*)[8]>(&h[0]));
+            ld_global_nc_v8(p.truth + 2 * g + 8, *reinterpret_cast<float(*)[8]>(&h[8]));
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float dx = o[2 * i] - h[2 * i], dy = o[2 * i + 1] - h[2 * i + 1];
+                const float sq = dx * dx + dy * dy;
+                s_sq += sq;
+                s_abs += sqrtf(sq);
+            }
+        }
+    } else {
+        float2* taps = reinterpret_cast<float2*>(p.taps);
+        const float2* truth = reinterpret_cast<const float2*>(p.truth);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (n_first + i < n_valid) {
+                taps[g + i] = make_float2(o[2 * i], o[2 * i + 1]);
+                if (truth != nullptr) {
+                    const float2 h = __ldg(truth + g + i);
+                    const float dx = o[2 * i] - h.x, dy = o[2 * i + 1] - h.y;
+                    const float sq = dx * dx + dy * dy;
+                    s_sq += sq;
+                    s_abs += sqrtf(sq);
+                }
+            }
+        }
+    }
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(FUSED ? kFusedThreads : kThreads, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -186,7 +329,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], FUSED ? 1 + kConvWarps : 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -196,7 +339,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&tm_in);
+        if (!FUSED) tma_prefetch(&tm_in);
         tma_prefetch(&tm_circ);
     }
     if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -210,9 +353,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 
     if (warp == 0) {
         if (lane == 0) {
-            // ===== TMA producer
+            // ===== TMA producer (circulant rows; plus packed samples when !FUSED)
             const uint64_t pol_in = policy_evict_first();
             const uint64_t pol_circ = policy_evict_last();
+            const uint32_t tx = FUSED ? p.stage_bytes - a_bytes : p.stage_bytes;
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -222,8 +366,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
                     uint8_t* sb = sa + a_bytes;
-                    mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
-                    tma_load_2d(sa, &tm_in, &full[stage], kb * kBK, mt * kBM, pol_in);
+                    mbar_arrive_expect_tx(&full[stage], tx);
+                    if (!FUSED) tma_load_2d(sa, &tm_in, &full[stage], kb * kBK, mt * kBM, pol_in);
                     tma_load_2d(sb, &tm_circ, &full[stage], kb * kBK, nt * p.bn, pol_circ);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
@@ -258,7 +402,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else {
+    } else if (warp < 6) {
         // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4
         const int quarter = warp & 3;
         int acc = 0;
@@ -280,41 +424,24 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
             const int n_valid = n_tx * p.l;
             const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
-            float2* taps = reinterpret_cast<float2*>(p.taps);
-            const float2* truth = reinterpret_cast<const float2*>(p.truth);
             float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
 
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.bn);
-            for (int c0 = 0; c0 < p.bn; c0 += 16) {
-                float v[16];
-                tmem_ld16(t_row + c0, v);
-                float x[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float send = odd ? v[i] : v[8 + i];
-                    x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
-                }
-                const int n_first = nt * p.bn + c0 + (odd ? 8 : 0);
-                if (row_ok) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int n = n_first + i;
-                        if (n < n_valid) {
-                            float2 e;
-                            e.x = (odd ? x[i] : v[i]) * p.inv_m;
-                            e.y = (odd ? v[8 + i] : x[i]) * p.inv_m;
-                            taps[out_base + n] = e;
-                            if (!isfinite(e.x) || !isfinite(e.y)) s_bad += 1.f;
-                            if (truth != nullptr) {
-                                const float2 h = __ldg(truth + out_base + n);
-                                const float dx = e.x - h.x, dy = e.y - h.y;
-                                const float sq = dx * dx + dy * dy;
-                                s_sq += sq;
-                                s_abs += sqrtf(sq);
-                            }
-                        }
-                    }
-                }
+            const int n_tile0 = nt * p.bn;
+            int c0 = 0;
+            for (; c0 + 32 <= p.bn; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32_nowait(t_row + c0, v);
+                tmem_wait_ld();
+                epi_slice(p, v, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                epi_slice(p, v + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
+                          s_sq, s_bad);
+            }
+            if (c0 < p.bn) {
+                uint32_t v[16];
+                tmem_ld16_nowait(t_row + c0, v);
+                tmem_wait_ld();
+                epi_slice(p, v, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
             }
             // TMEM stage fully read -> release it to the MMA warp.
             tc_fence_before();
@@ -350,6 +477,48 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     if (s_bad != 0.f) atomicAdd(&p.stats[f * 4 + 2], (double)s_bad);
                 }
             }
+        }
+    } else if (FUSED) {
+        // ===== converter warps: raw f32 (I,Q) -> fp16/bf16 swizzled A stage.
+        // Software-pipelined one K-block ahead so ~64 KB of loads are in flight per SM.
+        const int ct = (warp - 6) * 32 + lane;
+        const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const int jobs = my_tiles * p.k_blocks;
+        ConvTask bufA[kTasksPerThread], bufB[kTasksPerThread];
+        int stage = 0;
+        uint32_t phase = 0;
+        auto job_coords = [&](int j, int& mt, int& kb) {
+            const int ti = j / p.k_blocks;
+            kb = j - ti * p.k_blocks;
+            const int tile = blockIdx.x + ti * gridDim.x;
+            mt = tile / p.n_tiles;
+        };
+        auto load_job = [&](int j, ConvTask (&buf)[kTasksPerThread]) {
+            int mt, kb;
+            job_coords(j, mt, kb);
+#pragma unroll
+            for (int i = 0; i < kTasksPerThread; ++i) conv_load(p, mt, kb, i * kConvWarps * 32 + ct, buf[i]);
+        };
+        auto store_job = [&](ConvTask (&buf)[kTasksPerThread]) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+#pragma unroll
+            for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        };
+        if (jobs > 0) load_job(0, bufA);
+        int j = 0;
+        while (j < jobs) {
+            if (j + 1 < jobs) load_job(j + 1, bufB);
+            store_job(bufA);
+            ++j;
+            if (j >= jobs) break;
+            if (j + 1 < jobs) load_job(j + 1, bufA);
+            store_job(bufB);
+            ++j;
         }
     }
 
@@ -541,7 +710,9 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(k_correlate, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        attr_err = cudaFuncSetAttribute(k_correlate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_correlate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     });
     if (attr_err != cudaSuccess) {
         pnce_plan_destroy(p);
@@ -596,21 +767,17 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     return PNCE_OK;
 }
 
-pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
-                             double* stats, int64_t n_frames, void* stream) {
-    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
-    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
-    if (n_frames == 0) return PNCE_OK;
-    if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
-    if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
+// Shared launch setup for both K3 variants.
+static pnce_status_t fill_params(const pnce_plan_t* p, float* taps, const float* truth, double* stats,
+                                 int64_t n_frames, CorrParams& prm) {
     if ((reinterpret_cast<uintptr_t>(taps) & 7) || (truth && (reinterpret_cast<uintptr_t>(truth) & 7)))
         return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
     const pnce_cfg_t& c = p->cfg;
-    CorrParams prm{};
+    prm = CorrParams{};
     prm.total_rows = n_frames * p->n_batches * (int64_t)c.n_r * 2;
     const int64_t m_tiles = (prm.total_rows + kBM - 1) / kBM;
-    if (m_tiles * p->n_tiles > INT32_MAX) return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
-    if (prm.total_rows > INT32_MAX) return fail(PNCE_ERR_DIMENSION, "too many rows for one tensor map");
+    if (m_tiles * p->n_tiles > INT32_MAX || prm.total_rows > INT32_MAX)
+        return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
     prm.n_tiles = p->n_tiles;
     prm.bn = p->bn;
@@ -624,18 +791,34 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     prm.n_batches = p->n_batches;
     prm.n_batch = c.n_batch;
     prm.l = c.l;
+    prm.m = c.m;
+    prm.c = c.c;
+    prm.samples = c.c + c.m + c.l - 1;
+    prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
     prm.inv_m = 1.0f / (float)c.m;
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
-    CUtensorMap tm_in;
-    pnce_status_t s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, c.dtype == PNCE_DTYPE_BF16);
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
+                             double* stats, int64_t n_frames, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
+    if (n_frames == 0) return PNCE_OK;
+    if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
+    if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
+    CorrParams prm;
+    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
-    const int64_t tiles = m_tiles * p->n_tiles;
+    CUtensorMap tm_in;
+    s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
+    if (s != PNCE_OK) return s;
+    const int64_t tiles = (int64_t)prm.m_tiles * p->n_tiles;
     const int grid = (int)(tiles < p->num_sms ? tiles : p->num_sms);
     const size_t smem = 1024 + (size_t)p->stages * p->stage_bytes + 256;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    k_correlate<<<grid, kThreads, smem, st>>>(tm_in, p->tm_circ, prm);
+    k_correlate<false><<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(tm_in, p->tm_circ, prm);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;
@@ -644,13 +827,25 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
 pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                   double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
                                   void* stream) {
+    (void)workspace;
+    (void)workspace_bytes;
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
-    if (workspace_bytes < pnce_workspace_bytes(p, n_frames))
-        return fail(PNCE_ERR_DIMENSION, "workspace too small");
-    pnce_status_t s = pnce_pack_iq(p, iq, workspace, n_frames, stream);
+    if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
+    if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
+    CorrParams prm;
+    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
-    return pnce_correlate(p, workspace, taps, truth, stats, n_frames, stream);
+    prm.iq = iq;
+    const int64_t tiles = (int64_t)prm.m_tiles * p->n_tiles;
+    const int grid = (int)(tiles < p->num_sms ? tiles : p->num_sms);
+    const size_t smem = 1024 + (size_t)p->stages * p->stage_bytes + 256;
+    // tm_in is unused by the fused variant; pass the circulant map in its slot.
+    k_correlate<true><<<grid, kFusedThreads, smem, static_cast<cudaStream_t>(stream)>>>(p->tm_circ, p->tm_circ, prm);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return PNCE_OK;
 }
 
 }  // extern "C"

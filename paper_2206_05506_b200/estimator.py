@@ -101,7 +101,6 @@ class Correlator:
             _lib.check(L.pnce_plan_create(ctypes.byref(self._c), ctypes.byref(handle),
                                           _stream_ptr(self.device)))
         self._plan = handle
-        self._ws: torch.Tensor | None = None
 
     def __del__(self):
         plan = getattr(self, "_plan", None)
@@ -132,14 +131,9 @@ class Correlator:
                                                   _stream_ptr(self.device)))
         return out
 
-    def workspace_bytes(self, n_frames: int) -> int:
+    def packed_bytes(self, n_frames: int) -> int:
+        """Size of the packed 16-bit operand `pack` produces (the fused path needs none)."""
         return int(_lib.lib().pnce_workspace_bytes(self._plan, n_frames))
-
-    def workspace(self, n_frames: int) -> torch.Tensor:
-        need = self.workspace_bytes(n_frames)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
-        return self._ws
 
     # ------------------------------------------------------------ validation
     def _check_iq(self, iq: torch.Tensor) -> tuple[torch.Tensor, int]:
@@ -186,12 +180,10 @@ class Correlator:
             if tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64:
                 raise DimensionMismatchError("stats must be float64 (F, 4)")
             stats_ptr = ctypes.c_void_p(stats.data_ptr())
-        ws = self.workspace(n_frames)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().pnce_process_frames(
                 self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                truth_ptr, stats_ptr, ctypes.c_void_p(ws.data_ptr()), ws.numel(), n_frames,
-                _stream_ptr(self.device)))
+                truth_ptr, stats_ptr, None, 0, n_frames, _stream_ptr(self.device)))
         return out, stats
 
     def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64) -> torch.Tensor:
@@ -317,9 +309,11 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
     Correlator (the static state the reference passes as rows_per_batch).
     """
     dtype = backend or (rows_per_batch.dtype if rows_per_batch is not None else "fp16")
+    single = True
     if isinstance(frames, torch.Tensor):
         iq = frames
         n_r = int(frames.shape[-3])
+        single = frames.dim() == 4
     else:
         host = _frames_to_iq(frames, cfg)
         n_r = host.shape[2]
@@ -339,7 +333,6 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
     if counters is not None:
         counters.samples_moved += n_frames * cfg.n_batches * n_r * cfg.p
         counters.macs += n_frames * cfg.n_t * cfg.l * cfg.m * n_r
-    single = iq.dim() == 4
     out_taps = taps[0] if single else taps
     saturations = 0
     if stats is not None:
