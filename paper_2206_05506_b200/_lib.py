@@ -12,7 +12,7 @@ import os
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpnce_b200.so")
+LIB_PATH = os.environ.get("PNCE_LIB", os.path.join(_HERE, "lib", "libpnce_b200.so"))
 
 PNCE_DTYPE_FP16 = 0
 PNCE_DTYPE_BF16 = 1

@@ -248,3 +248,42 @@ def test_noiseless_bound_at_scale(dev):
     assert bool((err <= bound + slack).all())
     ref = oracle_est(chips, ocfg, iq[:1])
     assert link_err(taps[0, :1].cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_fused_variants_agree(dev, mode, monkeypatch):
+    """Both fused K3 variants (LDG converters / TMA-staged converters) match the oracle and
+    each other bit for bit (same quantisation, same MMA order)."""
+    n, m, l, nb = CONFIGS["cfg3"]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    chips, iq, _ = sim_sets(ocfg, 2)
+    corr = P.Correlator(P.default_spec(10), cfg, n, device=dev)
+    x = torch.from_numpy(iq).to(dev)
+    monkeypatch.setenv("PNCE_TUNE_FUSED_MODE", mode)
+    taps, _ = corr.process(x)
+    monkeypatch.delenv("PNCE_TUNE_FUSED_MODE")
+    ref_gpu, _ = corr.process(x)
+    assert torch.equal(taps, ref_gpu)
+    assert link_err(taps.cpu().numpy(), oracle_est(chips, ocfg, iq)) <= TOL
+
+
+def test_odd_row_stride(dev):
+    """C + L odd -> odd samples per row (8-byte aligned rows): exercises the LDG path."""
+    cfg, ocfg = make_cfg(16, 255, 32, 4, c=33)
+    assert cfg.samples_per_receiver % 2 == 1
+    chips, iq, _ = sim_sets(ocfg, 3)
+    corr = P.Correlator(P.default_spec(8), cfg, 16, device=dev)
+    taps, _ = corr.process(torch.from_numpy(iq).to(dev))
+    assert link_err(taps.cpu().numpy(), oracle_est(chips, ocfg, iq)) <= TOL
+
+
+def test_packed_path_matches_fused(dev):
+    """K2 (pack) + K3 on the packed operand == the fused kernel, bit for bit."""
+    n, m, l, nb = CONFIGS["cfg4p"]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    _, iq, _ = sim_sets(ocfg, 1)
+    corr = P.Correlator(P.default_spec(11), cfg, n, device=dev)
+    x = torch.from_numpy(iq).to(dev)
+    fused, _ = corr.process(x)
+    packed, _ = corr.correlate(corr.pack(x), 1)
+    assert torch.equal(fused, packed)
