@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/pnce_b200.h"
 #include "sm100_ptx.cuh"
@@ -39,7 +40,6 @@ namespace {
 constexpr int kBM = 128;       // UMMA M (input rows per tile)
 constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
 constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
-constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
 constexpr int kSmemLimit = 227 * 1024;
 
 thread_local std::string g_err;
@@ -81,11 +81,11 @@ __global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* ch
 // Stacked lag-window rows, K-major, zero padded: A[n, k] for n < rows_alloc, k < k_pad.
 template <typename T>
 __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m,
-                                  int k_pad, int r_total, int rows_alloc, int l, int spacing) {
+                                  int k_pad, int r_total, int rows_alloc, int l, int spacing, int repl) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)rows_alloc * k_pad;
+    int64_t total = (int64_t)rows_alloc * k_pad * repl;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-        int n = (int)(idx / k_pad);
+        int n = (int)((idx / k_pad) % rows_alloc);
         int k = (int)(idx % k_pad);
         float v = 0.0f;
         if (n < r_total && k < m) {
@@ -152,22 +152,49 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
 }
 
 // ------------------------------------------------------------------ K3+K4
-// Correlation kernel.  The fused variants read the raw f32 (I,Q) frames directly: eight
-// converter warps perform remove_cp + de-interleave + fp16/bf16 quantisation
-// straight into the 128B-swizzled UMMA A stage (K2 fused away, no packed
-// intermediate in HBM).  The packed variant consumes the K2 operand through TMA.
-constexpr int kConvWarps = 8;                       // converter warps per CTA
-constexpr int kConvGroups = 2;                      // groups alternate K-blocks (2 jobs in flight)
-constexpr int kGroupWarps = kConvWarps / kConvGroups;
-constexpr int kFusedThreads = (6 + kConvWarps) * 32;
-constexpr int kRawThreads = (7 + kConvWarps) * 32;  // + raw-sample TMA producer warp
-
-// K3 variants: 0 = packed 16-bit operand via TMA; 1 = fused, converter warps load f32
-// with LDG; 2 = fused, f32 rows TMA-staged in shared memory, converters LDS -> STS.
+// Correlation kernel, one CTA pair (cluster 2x1, tcgen05 cta_group::2) per 256 input
+// rows.  Variants (template MODE):
+//   kModePacked   : rows = the packed 16-bit operand of K2, TMA-loaded;
+//   kModeFusedTma : rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
+//                   converted (remove_cp + de-interleave + fp16/bf16) by converter warps
+//                   straight into the 128B-swizzled UMMA A stage -- K2 fused away;
+//   kModeFusedLdg : as above but converters LDG the f32 rows (fallback for row strides
+//                   that are not 16-byte multiples).
+// Warp roles (16 warps, both CTAs unless noted):
+//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader) / arrive forwarder (peer)
+//   2 raw-row TMA producer (FusedTma)                3 spare
+//   4-7 converters (fused)                           8-15 epilogue (2 warps per TMEM lane quarter)
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
-constexpr int kLinksPerTile = kBM / 2;                                         // 64 (re, im) row pairs
-constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kGroupWarps * 32);  // 4
-constexpr uint32_t kRawStageBytes = kLinksPerTile * kBK * 8;  // 64 links x 64 (I,Q) f32 = 32 KB
+
+#ifdef PNCE_DIAG_TRACE
+// Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
+constexpr int kTraceSlots = 16, kTraceMax = 512;
+__device__ long long g_trace[2 * kTraceSlots * kTraceMax];
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(slot, idx)                                                                   \
+    do {                                                                                   \
+        if (blockIdx.x < 2 && (idx) < kTraceMax)                                           \
+            g_trace[(blockIdx.x * kTraceSlots + (slot)) * kTraceMax + (idx)] = gtimer();  \
+    } while (0)
+#else
+#define TRACE(slot, idx) \
+    do {                 \
+    } while (0)
+#endif
+constexpr int kWarps = 16;
+constexpr int kThreadsK3 = kWarps * 32;
+constexpr int kConvWarp0 = 4;
+constexpr int kConvWarps = 4;
+constexpr int kEpiWarp0 = 8;
+constexpr int kEpiWarps = 8;
+constexpr int kLinksPerTile = kBM / 2;                                        // 64 (re, im) row pairs
+constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
+constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
+constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;         // 64 links: 33 KB
 
 struct CorrParams {
     int64_t total_rows;  // n_frames * n_batches * n_r * 2
@@ -179,13 +206,15 @@ struct CorrParams {
     int32_t acc_stages;  // TMEM accumulator buffers (2 if 2*g_cols <= 512)
     int32_t k_blocks;
     int32_t stages;
-    int32_t raw_stages;  // MODE 2: f32 staging ring depth
+    int32_t raw_stages;  // FusedTma: f32 staging ring depth
+    int32_t circ_repl;   // circulant replicas
+    int32_t circ_rows;   // rows per replica
     uint32_t stage_bytes;
     uint32_t tx_bytes;   // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
-    int32_t m, c, samples;  // PN length, CP length, samples per received row (fused input)
+    int32_t m, c, samples;  // PN length, CP length, samples per received row
     int32_t bf16;
     float inv_m;
     const float* iq;
@@ -194,7 +223,7 @@ struct CorrParams {
     double* stats;
 };
 
-// One converter task: 8 consecutive body samples of one link -> 16 B of Re, 16 B of Im.
+// One LDG-converter task: 8 consecutive body samples of one link.
 struct ConvTask {
     float re[8], im[8];
 };
@@ -205,37 +234,13 @@ __device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, in
     const int64_t q = link0 + link_local;
     const int k0 = kb * kBK + chunk * 8;
     const int64_t total_links = p.total_rows >> 1;
-    if (q < total_links && k0 + 8 <= p.m) {
-        const int64_t s0 = q * p.samples + p.c + k0;  // complex index
-        const float* src = p.iq + 2 * s0;
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            const float4* s4 = reinterpret_cast<const float4*>(src);
+    const bool ok = q < total_links;
+    const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float4 v = __ldg(s4 + j);
-                t.re[2 * j] = v.x;
-                t.im[2 * j] = v.y;
-                t.re[2 * j + 1] = v.z;
-                t.im[2 * j + 1] = v.w;
-            }
-        } else {
-            const float2* s2 = reinterpret_cast<const float2*>(src);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float2 v = __ldg(s2 + j);
-                t.re[j] = v.x;
-                t.im[j] = v.y;
-            }
-        }
-    } else {
-        const bool ok = q < total_links;
-        const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float2 v = (ok && k0 + j < p.m) ? __ldg(s2 + j) : make_float2(0.f, 0.f);
-            t.re[j] = v.x;
-            t.im[j] = v.y;
-        }
+    for (int j = 0; j < 8; ++j) {
+        const float2 v = (ok && k0 + j < p.m) ? __ldg(s2 + j) : make_float2(0.f, 0.f);
+        t.re[j] = v.x;
+        t.im[j] = v.y;
     }
 }
 
@@ -248,11 +253,15 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__device__ __forceinline__ void conv_store(uint8_t* stage_a, int task, const ConvTask& t, int bf16) {
+// 128B swizzle of the UMMA K-major A stage: 16-byte chunk c of row r lives at chunk c ^ (r % 8).
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row) {
+    return base + row * 128 + ((((byte_in_row >> 4) ^ (row & 7))) << 4) + (byte_in_row & 15);
+}
+
+__device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask& t, int bf16) {
     const int link_local = task >> 3;
     const int chunk = task & 7;
-    const int row_re = 2 * link_local;
-    const int row_im = row_re + 1;
+    const int row_re = 2 * link_local, row_im = row_re + 1;
     uint4 vr, vi;
     vr.x = pack2(t.re[0], t.re[1], bf16);
     vr.y = pack2(t.re[2], t.re[3], bf16);
@@ -262,10 +271,8 @@ __device__ __forceinline__ void conv_store(uint8_t* stage_a, int task, const Con
     vi.y = pack2(t.im[2], t.im[3], bf16);
     vi.z = pack2(t.im[4], t.im[5], bf16);
     vi.w = pack2(t.im[6], t.im[7], bf16);
-    // 128B swizzle: 16-byte chunk c of row r lives at chunk position c ^ (r % 8)
-    const uint32_t base = smem_u32(stage_a);
-    st_shared_v4(base + row_re * 128 + ((chunk ^ (row_re & 7)) << 4), vr);
-    st_shared_v4(base + row_im * 128 + ((chunk ^ (row_im & 7)) << 4), vi);
+    st_shared_v4(swz(sa, row_re, chunk * 16), vr);
+    st_shared_v4(swz(sa, row_im, chunk * 16), vi);
 }
 
 // Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
@@ -286,9 +293,11 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
         o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
     }
+    if (p.stats != nullptr) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
+        for (int i = 0; i < 8; ++i)
+            if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
+    }
     const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
 #ifdef PNCE_DIAG_NO_STORE
     if (o[0] == 12345.678f) p.taps[g] = o[1];  // keep the work, drop the stores
@@ -329,20 +338,16 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
     }
 }
 
-// CTA pair (cluster 2x1): the pair owns 256 input rows (128 per CTA, UMMA M = 256,
-// cta_group::2); the leader CTA (rank 0) issues every MMA, each CTA supplies its
-// half of the circulant rows (B is split along N) and its own 128 sample rows.
 template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1)
-__launch_bounds__(MODE == kModePacked ? kThreads : (MODE == kModeFusedLdg ? kFusedThreads : kRawThreads), 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
     constexpr bool FUSED = MODE != kModePacked;
     constexpr bool RAW = MODE == kModeFusedTma;
-    constexpr int kConvWarp0 = RAW ? 7 : 6;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
+    // [A/B stages][1 KB barrier block][raw f32 stages]
     const int S = p.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
     uint64_t* empty = full + S;
@@ -351,25 +356,23 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     uint64_t* raw_full = tempty + 2;
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
-    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;  // after the barrier block
+    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
-    constexpr int kConvPerJob = MODE == kModeFusedLdg ? kGroupWarps : kConvWarps;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            // FUSED: the leader's full barrier takes its producer's expect_tx arrive, one
-            // arrive per local converter warp and one forwarded arrive from the peer CTA;
-            // the peer's full barrier only collects its own converter warps.
-            mbar_init(&full[s], FUSED ? (leader ? 2 + kConvPerJob : kConvPerJob) : 1);
+            // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
+            // bytes and converter arrives land on the leader's barrier).
+            mbar_init(&full[s], FUSED ? 1 + 2 * kConvWarps : 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);
+            mbar_init(&tempty[a], 2 * kEpiWarps);
         }
         if (RAW) {
             for (int s = 0; s < p.raw_stages; ++s) {
@@ -392,91 +395,182 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int n_clusters = gridDim.x >> 1;
     const int cid = blockIdx.x >> 1;
     const int total_tiles = p.m_tiles * p.n_groups;
+    const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
+    const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
     const uint32_t a_bytes = kBM * kBK * 2;
     const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ===== TMA producer (both CTAs; transaction bytes land on the leader's barrier)
+            // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
             const uint64_t pol_in = policy_evict_first();
             const uint64_t pol_circ = policy_evict_last();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = cid; tile < total_tiles; tile += n_clusters) {
+            const int circ_row0 = (cid % p.circ_repl) * p.circ_rows;
+            for (int j = 0; j < jobs; ++j) {
+                const int ti = j / p.k_blocks;
+                const int kb = j - ti * p.k_blocks;
+                const int tile = cid + ti * n_clusters;
                 const int mt = tile / p.n_groups;
                 const int g = tile - mt * p.n_groups;
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
-                    uint8_t* sb = sa + a_bytes;
-                    const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-                    if (!FUSED)
-                        tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
-                    for (int j = 0; j < p.n_mma; ++j)
-                        tma_load_2d_pair(sb + j * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
-                                         g * p.g_cols + j * p.nm + (int)rank * (p.nm / 2), pol_circ);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
+                const int stage = j % S;
+                mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+                TRACE(0, j);
+                uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+                uint8_t* sb = sa + a_bytes;
+                const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
+                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
+                if (!FUSED)
+                    tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
+                for (int jj = 0; jj < p.n_mma; ++jj)
+                    tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
+                                     circ_row0 + g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
             }
         }
     } else if (warp == 1) {
-        if (FUSED && !leader && lane == 0) {
-            // ===== peer CTA: forward "converted samples landed" to the leader's full barrier.
-            // The converters arrive locally (CTA-scope release, no fence stall on their
-            // in-flight prefetch loads); this thread has no outstanding loads, so its
-            // cluster-scope release is cheap and transitively covers their smem writes.
-            int stage = 0;
-            uint32_t phase = 0;
-            const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
-            const int jobs = my_tiles * p.k_blocks;
-            for (int j = 0; j < jobs; ++j) {
-                mbar_wait(&full[stage], phase);
-                mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
-                if (++stage == S) { stage = 0; phase ^= 1; }
-            }
-        }
         if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
-            int stage = 0;
-            uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = cid; tile < total_tiles; tile += n_clusters) {
-                mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+            for (int ti = 0; ti < my_tiles; ++ti) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                TRACE(1, ti);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    if (FUSED) mbar_wait_cluster(&full[stage], phase);
-                    else mbar_wait(&full[stage], phase);
+                    const int j = ti * p.k_blocks + kb;
+                    const int stage = j % S;
+                    const uint32_t phase = (uint32_t)(j / S) & 1u;
+#ifndef PNCE_DIAG_NO_FULLWAIT
+                    mbar_wait(&full[stage], phase);
+#else
+                    (void)phase;
+#endif
+                    TRACE(2, j);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
                     const uint32_t sb = sa + a_bytes;
 #pragma unroll
                     for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
-                        for (int j = 0; j < p.n_mma; ++j) {
-                            const uint64_t bd = make_sdesc(sb + j * b_half_bytes + ks * 32, 16, 1024, 2);
-                            umma_f16_ss_pair(d_tmem + (uint32_t)(j * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
+                        for (int jj = 0; jj < p.n_mma; ++jj) {
+                            const uint64_t bd = make_sdesc(sb + jj * b_half_bytes + ks * 32, 16, 1024, 2);
+                            umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
                         }
                     }
                     umma_commit_pair(&empty[stage]);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
+                    TRACE(3, j);
                 }
                 umma_commit_pair(&tfull[acc]);
                 if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else if (warp < 6) {
-        // ===== epilogue warps 2..5 (both CTAs): TMEM lane quarter = warp % 4
+    } else if (warp == 2) {
+        if (RAW && lane == 0) {
+            // ===== raw-row producer: TMA the f32 (I,Q) rows of this CTA's 64 links for one
+            // K-block (64 links x 64 samples x 8 B = 32 KB) into the staging ring.
+            const uint64_t pol = policy_evict_first();
+            for (int j = 0; j < jobs; ++j) {
+                const int ti = j / p.k_blocks;
+                const int kb = j - ti * p.k_blocks;
+                const int mt = (cid + ti * n_clusters) / p.n_groups;
+                const int rs = j % p.raw_stages;
+                mbar_wait(&raw_empty[rs], ((uint32_t)(j / p.raw_stages) & 1u) ^ 1u);
+                TRACE(6, j);
+#ifdef PNCE_DIAG_NO_RAW
+                mbar_arrive(&raw_full[rs]);
+                (void)pol; (void)mt; (void)kb;
+#else
+                mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
+                // box start rounded down to a 16-byte boundary; converters skip the slack
+                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs],
+                            (2 * (p.c + kb * kBK)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile, pol);
+#endif
+            }
+        }
+    } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
+        if (FUSED) {
+            const int cw = warp - kConvWarp0;
+            for (int j = 0; j < jobs; ++j) {
+                const int ti = j / p.k_blocks;
+                const int kb = j - ti * p.k_blocks;
+                const int stage = j % S;
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                if (RAW) {
+                    // staged f32 rows -> A stage.  Warp w converts links w, w+4, ...; lane l
+                    // handles samples 2l, 2l+1 (one conflict-free LDS.128 of the 512 B row,
+                    // two STS.32 into the Re / Im rows).
+                    const int rs = j % p.raw_stages;
+                    mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
+                    if (cw == 0 && lane == 0) TRACE(7, j);
+                    mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+                    if (cw == 0 && lane == 0) TRACE(8, j);
+                    const int slack = (2 * (p.c + kb * kBK)) & 3;  // 0 or 2 floats
+                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * kRawStageBytes) + slack * 4 + lane * 16;
+                    const int k = kb * kBK + 2 * lane;
+                    const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
+#ifndef PNCE_DIAG_NO_CONV
+#pragma unroll 4
+                    for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
+                        const int link_local = cw + kConvWarps * i;
+                        float4 v;
+                        if (slack == 0) {
+                            v = ld_shared_v4f(raw + link_local * (kRawRowFloats * 4));
+                        } else {
+                            const float2 a = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4));
+                            const float2 b = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4) + 8);
+                            v = make_float4(a.x, a.y, b.x, b.y);
+                        }
+                        if (!ok0) { v.x = 0.f; v.y = 0.f; }
+                        if (!ok1) { v.z = 0.f; v.w = 0.f; }
+                        st_shared_u32(swz(sa, 2 * link_local, lane * 4), pack2(v.x, v.z, p.bf16));
+                        st_shared_u32(swz(sa, 2 * link_local + 1, lane * 4), pack2(v.y, v.w, p.bf16));
+                    }
+#else
+                    (void)raw; (void)ok0; (void)ok1;
+#endif
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        // proxy fence above completed this warp's STS; plain (CTA-scope
+                        // release) arrive on the leader's barrier, no GPU-scope membar
+                        mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                        mbar_arrive(&raw_empty[rs]);
+                        if (cw == 0) TRACE(9, j);
+                    }
+                } else {
+                    // LDG fallback: 4 tasks (link, 8-sample chunk) per thread
+                    const int mt = (cid + ti * n_clusters) / p.n_groups;
+                    const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
+                    const int ct = cw * 32 + lane;
+                    ConvTask buf[kTasksPerThread];
+#pragma unroll
+                    for (int i = 0; i < kTasksPerThread; ++i)
+                        conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
+                    mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+#pragma unroll
+                    for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                }
+            }
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ===== epilogue (both CTAs): TMEM lane quarter = warp % 4, column half = (warp-8)/4
         const int quarter = warp & 3;
+        const int half = (warp - kEpiWarp0) >> 2;
+        const int cph = ((p.g_cols + 1) / 2 + 15) / 16 * 16;
+        const int c_begin = min(p.g_cols, half * cph);
+        const int c_end = min(p.g_cols, c_begin + cph);
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = cid; tile < total_tiles; tile += n_clusters) {
+        for (int ti = 0; ti < my_tiles; ++ti) {
+            const int tile = cid + ti * n_clusters;
             const int mt = tile / p.n_groups;
             const int g = tile - mt * p.n_groups;
             mbar_wait(&tfull[acc], acc_phase);
+            if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
             tc_fence_after();
 
             const int64_t row = (int64_t)mt * 2 * kBM + (int64_t)rank * kBM + quarter * 32 + lane;
@@ -494,25 +588,43 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.g_cols);
             const int n_tile0 = g * p.g_cols;
-            int c0 = 0;
-            for (; c0 + 32 <= p.g_cols; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32_nowait(t_row + c0, v);
+            // 32-column chunks (two 16-column slices each); the next chunk's TMEM load is
+            // in flight while the current one is paired, scaled and stored.
+            uint32_t va[32], vb[32];
+            int c0 = c_begin;
+            if (c0 + 32 <= c_end) {
+                tmem_ld32_nowait(t_row + c0, va);
                 tmem_wait_ld();
-                epi_slice(p, v, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
-                epi_slice(p, v + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
-                          s_sq, s_bad);
+                while (true) {
+                    const bool more = c0 + 64 <= c_end;
+                    if (more) tmem_ld32_nowait(t_row + c0 + 32, vb);
+                    epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
+                              s_sq, s_bad);
+                    c0 += 32;
+                    if (!more) break;
+                    tmem_wait_ld();
+                    const bool more2 = c0 + 64 <= c_end;
+                    if (more2) tmem_ld32_nowait(t_row + c0 + 32, va);
+                    epi_slice(p, vb, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
+                              s_sq, s_bad);
+                    c0 += 32;
+                    if (!more2) break;
+                    tmem_wait_ld();
+                }
             }
-            if (c0 < p.g_cols) {
-                uint32_t v[16];
-                tmem_ld16_nowait(t_row + c0, v);
+            if (c0 < c_end) {  // 16-column remainder
+                tmem_ld16_nowait(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(va));
                 tmem_wait_ld();
-                epi_slice(p, v, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
             }
-            // this CTA's half of the accumulator is drained -> tell the leader's MMA warp
+            // this warp's share of the accumulator is drained -> tell the leader's MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
+            if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
+            if (lane == 0 && warp == kEpiWarp0 + kEpiWarps - 1) TRACE(12, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
 
             if (p.stats != nullptr) {
@@ -542,89 +654,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     }
                     if (s_bad != 0.f) atomicAdd(&p.stats[f * 4 + 2], (double)s_bad);
                 }
-            }
-        }
-    } else if (MODE == kModeFusedLdg) {
-        // ===== converter warps (both CTAs): raw f32 (I,Q) -> fp16/bf16 swizzled A stage of
-        // this CTA's 128 rows.  Two groups of warps alternate K-blocks; each group issues
-        // the loads of its next job only after publishing the current one, so the
-        // proxy fence before the arrive never waits on in-flight prefetches, and the
-        // two groups keep two K-blocks (64 KB) of loads in flight per SM.
-        const int cw = warp - 6;
-        const int grp = cw / kGroupWarps;
-        const int ct = (cw % kGroupWarps) * 32 + lane;
-        const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
-        const int jobs = my_tiles * p.k_blocks;
-        ConvTask buf[kTasksPerThread];
-        for (int j = grp; j < jobs; j += kConvGroups) {
-            const int ti = j / p.k_blocks;
-            const int kb = j - ti * p.k_blocks;
-            const int tile = cid + ti * n_clusters;
-            const int mt = tile / p.n_groups;
-            const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
-#pragma unroll
-            for (int i = 0; i < kTasksPerThread; ++i) conv_load(p, link0, kb, i * kGroupWarps * 32 + ct, buf[i]);
-            const int stage = j % S;
-            const uint32_t phase = (uint32_t)(j / S) & 1u;
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
-#pragma unroll
-            for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kGroupWarps * 32 + ct, buf[i], p.bf16);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[stage]);  // CTA-local; the peer forwards (see warp 1)
-        }
-    } else if (RAW && warp == 6) {
-        // ===== raw-sample producer (both CTAs): TMA the f32 (I,Q) rows of this CTA's 64
-        // links for one K-block (64 links x 64 samples x 8 B = 32 KB) into the staging ring.
-        if (lane == 0) {
-            const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
-            const int jobs = my_tiles * p.k_blocks;
-            const uint64_t pol = policy_evict_first();
-            for (int j = 0; j < jobs; ++j) {
-                const int ti = j / p.k_blocks;
-                const int kb = j - ti * p.k_blocks;
-                const int mt = (cid + ti * n_clusters) / p.n_groups;
-                const int rs = j % p.raw_stages;
-                mbar_wait(&raw_empty[rs], ((uint32_t)(j / p.raw_stages) & 1u) ^ 1u);
-                mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
-                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs], 2 * (p.c + kb * kBK),
-                            (mt * 2 + (int)rank) * kLinksPerTile, pol);
-            }
-        }
-    } else if (RAW) {
-        // ===== converters (both CTAs): staged f32 rows -> fp16/bf16 swizzled A stage.
-        // Warp w converts links w, w+8, ...; lane l handles samples 2l, 2l+1 of a link
-        // (one conflict-free LDS.128 of the 512 B row, two STS.32 into the Re / Im rows).
-        const int cw = warp - kConvWarp0;
-        const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
-        const int jobs = my_tiles * p.k_blocks;
-        for (int j = 0; j < jobs; ++j) {
-            const int kb = j % p.k_blocks;
-            const int rs = j % p.raw_stages;
-            const int stage = j % S;
-            mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
-            mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
-            const uint32_t raw = smem_u32(raw_base + (size_t)rs * kRawStageBytes);
-            const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-            const int k = kb * kBK + 2 * lane;
-            const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
-#pragma unroll
-            for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
-                const int link_local = cw + kConvWarps * i;
-                float4 v = ld_shared_v4f(raw + link_local * (kBK * 8) + lane * 16);
-                if (!ok0) { v.x = 0.f; v.y = 0.f; }
-                if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                const int row_re = 2 * link_local, row_im = row_re + 1;
-                const int chunk = lane >> 2, within = (lane & 3) * 4;
-                st_shared_u32(sa + row_re * 128 + ((chunk ^ (row_re & 7)) << 4) + within, pack2(v.x, v.z, p.bf16));
-                st_shared_u32(sa + row_im * 128 + ((chunk ^ (row_im & 7)) << 4) + within, pack2(v.y, v.w, p.bf16));
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&full[stage]);       // CTA-local; the peer forwards (see warp 1)
-                mbar_arrive(&raw_empty[rs]);
             }
         }
     }
@@ -670,14 +699,15 @@ pnce_status_t make_tmap(CUtensorMap* map, const void* base, uint64_t cols, uint6
     return PNCE_OK;
 }
 
-// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][128 floats]
-// (= one K-block of 64 (I,Q) samples for 64 links), no swizzle.
+// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][132 floats]
+// (one K-block of 64 (I,Q) samples for 64 links + 16 B slack so the box start can be
+// rounded down to a 16-byte boundary), no swizzle.
 pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {row_floats, rows};
     cuuint64_t strides[1] = {row_floats * 4};
-    cuuint32_t box[2] = {(cuuint32_t)(2 * kBK), (cuuint32_t)kLinksPerTile};
+    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, (cuuint32_t)kLinksPerTile};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -706,7 +736,9 @@ struct pnce_plan {
     int n_batches;
     int r_total;     // N_b * L
     int k_pad;       // roundup(M, 64)
-    int rows_alloc;  // circulant rows allocated (>= both tilings' coverage)
+    int rows_alloc;  // circulant rows per replica (>= both tilings' coverage)
+    int repl;        // circulant replicas: CTA pairs spread their B loads over replicas so
+                     // the whole grid does not hammer the same L2 lines in lock-step
     int num_sms;
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
     Tiling packed;   // packed operand in: groups of <= 256 cols, double-buffered accumulator
@@ -823,7 +855,9 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
+    const char* rp = std::getenv("PNCE_TUNE_CIRC_REPL");
+    p->repl = std::max(1, std::min(64, rp ? std::atoi(rp) : 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2 * p->repl);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
@@ -834,14 +868,14 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         return s;
     }
     const int spacing = cfg->m / cfg->n_batch;
-    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad * p->repl;
     const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     if (cfg->dtype == PNCE_DTYPE_BF16)
         k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
+            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
     else
         k_build_circulant<__half><<<blocks, 256, 0, st>>>(
-            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
+            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
     g_launches++;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -849,9 +883,10 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
     }
-    s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, p->rows_alloc, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
+    const uint64_t circ_rows = (uint64_t)p->rows_alloc * p->repl;
+    s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
     if (s == PNCE_OK)
-        s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, p->rows_alloc, p->packed.nm / 2,
+        s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
                       cfg->dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
@@ -934,6 +969,8 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     if (m_tiles * t.n_groups > INT32_MAX || prm.total_rows > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
+    prm.circ_repl = p->repl;
+    prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
     prm.g_cols = t.g_cols;
     prm.n_mma = t.n_mma;
@@ -982,7 +1019,7 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) return s;
     const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-    k_correlate<kModePacked><<<pair_grid(p, prm), kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, static_cast<cudaStream_t>(stream)>>>(
         tm_in, p->packed.tm_circ, prm);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
@@ -1023,11 +1060,22 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         if (s != PNCE_OK) return s;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
                             (size_t)prm.raw_stages * kRawStageBytes;
-        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kRawThreads, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
+        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
+#ifdef PNCE_DIAG_TRACE
+        if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
+            static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
+            cudaStreamSynchronize(st);
+            cudaMemcpyFromSymbol(host.data(), g_trace, host.size() * sizeof(long long));
+            if (FILE* fh = std::fopen(tf, "wb")) {
+                std::fwrite(host.data(), sizeof(long long), host.size(), fh);
+                std::fclose(fh);
+            }
+        }
+#endif
     } else {
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         // tm_in is unused by the LDG-fused variant; pass the circulant map in its slot.
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kFusedThreads, smem, st>>>(p->fused.tm_circ,
+        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(p->fused.tm_circ,
                                                                                    p->fused.tm_circ, prm);
     }
     g_launches++;

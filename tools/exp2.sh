@@ -1,5 +1,5 @@
 #!/bin/bash
-A="--frames 4096 --gemm-frames 4096 --steps 5 --no-e2e --no-cpu"
+A="--frames 4096 --gemm-frames 1024 --steps 5 --no-e2e --no-cpu"
 run() { echo "== $1"; shift; env "$@" timeout -s KILL 200 python bench.py $A 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
@@ -8,10 +8,9 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l.strip()[:200])
 "; }
 run default X=1
-run ldg PNCE_TUNE_FUSED_MODE=1
 run raw3 PNCE_TUNE_RAW_STAGES=3
-
-run raw4ab2 PNCE_TUNE_RAW_STAGES=4 PNCE_TUNE_AB_STAGES=2
-run packed512 PNCE_TUNE_GROUP_PACKED=512
-run nostore PNCE_LIB=tools/bin/libpnce_diag_nostore.so
-run nostore_raw3 PNCE_LIB=tools/bin/libpnce_diag_nostore.so PNCE_TUNE_RAW_STAGES=3
+run no_store PNCE_LIB=tools/bin/libpnce_diag_no_store.so
+run pipe_only PNCE_LIB=tools/bin/libpnce_diag_pipe_only.so
+T="--frames 4096 --steps 1 --warmup 3 --no-gemm-leg --no-e2e --no-cpu"
+PNCE_LIB=tools/bin/libpnce_diag_trace.so PNCE_TRACE_FILE=gpurun_out/trace_full.bin python bench.py $T > /dev/null
+PNCE_LIB=tools/bin/libpnce_diag_trace_pipe.so PNCE_TRACE_FILE=gpurun_out/trace_pipe.bin python bench.py $T > /dev/null

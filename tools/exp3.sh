@@ -1,0 +1,18 @@
+#!/bin/bash
+A="--frames 4096 --gemm-frames 2048 --steps 5 --no-e2e --no-cpu"
+run() { echo "== $1"; shift; env "$@" timeout -s KILL 200 python bench.py $A 2>&1 | python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('fused us/frame %.3f  hbm %.1f%%  tensor %.1f%% | gemm us/frame %.3f tensor %.1f%%'%(d['us_per_frame'],100*d['roofline']['frac'],100*d['roofline']['tensor_frac'],d['gemm_leg']['us_per_frame'],100*d['gemm_leg']['frac_of_bf16_peak']))
+    elif 'Error' in l or 'error' in l: print(l.strip()[:200])
+"; }
+run repl1 PNCE_TUNE_CIRC_REPL=1
+run repl8 PNCE_TUNE_CIRC_REPL=8
+run repl32 PNCE_TUNE_CIRC_REPL=32
+run pipe_repl1 PNCE_TUNE_CIRC_REPL=1 PNCE_LIB=tools/bin/libpnce_diag_pipe_only.so
+run pipe_repl8 PNCE_TUNE_CIRC_REPL=8 PNCE_LIB=tools/bin/libpnce_diag_pipe_only.so
+run pipe_repl32 PNCE_TUNE_CIRC_REPL=32 PNCE_LIB=tools/bin/libpnce_diag_pipe_only.so
+run nostore_repl8 PNCE_TUNE_CIRC_REPL=8 PNCE_LIB=tools/bin/libpnce_diag_no_store.so
+T="--frames 4096 --steps 1 --warmup 3 --no-gemm-leg --no-e2e --no-cpu"
+PNCE_LIB=tools/bin/libpnce_diag_trace_pipe.so PNCE_TRACE_FILE=gpurun_out/trace_pipe8.bin python bench.py $T > /dev/null

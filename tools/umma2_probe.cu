@@ -27,26 +27,13 @@ using namespace pnce;
         }                                                                                       \
     } while (0)
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
+__device__ __forceinline__ uint32_t cluster_rank() { return cluster_ctarank(); }
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) { return mapa_shared(addr, rank); }
+__device__ __forceinline__ void mbar_arrive_remote_rel(uint32_t a) { mbar_arrive_cluster(a); }
 
 constexpr int NMAX = 256;
 // smem: A 16 KB | B (NMAX/2 rows x 128 B) 16 KB | bars
-template <int N>
+template <int N, int VAR = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 k_probe2(const __half* __restrict__ a_full, const __half* __restrict__ b_full, int iters, long long* cycles,
          float* d_out) {
@@ -72,6 +59,7 @@ k_probe2(const __half* __restrict__ a_full, const __half* __restrict__ b_full, i
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 2);
+        mbar_init(&bar[2], 1 << 20);
         fence_mbar_init();
     }
     fence_proxy_async_smem();
@@ -85,20 +73,27 @@ k_probe2(const __half* __restrict__ a_full, const __half* __restrict__ b_full, i
     const uint32_t tmem = *slot;
 
     // remote arrive test: both CTAs arrive on rank 0's bar[1]
-    if (tid == 0) mbar_arrive_remote(mapa(smem_u32(&bar[1]), 0));
+    if (tid == 0) mbar_arrive_remote_rel(mapa(smem_u32(&bar[1]), 0));
 
     const uint32_t idesc = make_idesc_f16(256, N, 0);
     if (rank == 0 && warp == 1 && lane == 0) {
         mbar_wait(&bar[1], 0);
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
-            const int ks = it & 3;
+            int ks = it & 3;
+            uint32_t dcol = 0;
+            if (VAR == 1) { ks = (it >> 1) & 3; dcol = (it & 1) * 256; }          // alternate accumulators
+            if (VAR == 2) { ks = it & 3; dcol = ((it >> 2) & 1) * 256; }          // 4 then switch
             const uint64_t ad = make_sdesc(smem_u32(sA) + ks * 32, 16, 1024, 2);
             const uint64_t bd = make_sdesc(smem_u32(sB) + ks * 32, 16, 1024, 2);
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)(it > 0)) : "memory");
+                ::"r"(tmem + dcol), "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)(it > 1)) : "memory");
+            if (VAR >= 1 && (it & 7) == 7)
+                asm volatile(
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                    ::"r"(smem_u32(&bar[2])), "h"((uint16_t)3) : "memory");
         }
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -125,7 +120,7 @@ k_probe2(const __half* __restrict__ a_full, const __half* __restrict__ b_full, i
     }
 }
 
-template <int N>
+template <int N, int VAR = 0>
 void run(int nsm) {
     const int M = 256, K = 64;
     std::vector<__half> a(M * K), b(N * K);
@@ -143,8 +138,8 @@ void run(int nsm) {
     CK(cudaMemcpy(da, a.data(), a.size() * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
     const int smem = 32768 + 128 + 1024;
-    CK(cudaFuncSetAttribute(k_probe2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 160000));
-    k_probe2<N><<<2, 128, smem + 160000>>>(da, db, 4, dc, dd);   // big smem -> 1 CTA per SM
+    CK(cudaFuncSetAttribute(k_probe2<N, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + 160000));
+    k_probe2<N, VAR><<<2, 128, smem + 160000>>>(da, db, 4, dc, dd);   // big smem -> 1 CTA per SM
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<float> d(256 * NMAX);
@@ -158,7 +153,7 @@ void run(int nsm) {
             mx = fmax(mx, fabs(ref));
         }
     const int iters = 8192;
-    k_probe2<N><<<nsm, 128, smem + 160000>>>(da, db, iters, dc, dd);
+    k_probe2<N, VAR><<<nsm, 128, smem + 160000>>>(da, db, iters, dc, dd);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<long long> c(nsm / 2);
@@ -166,7 +161,7 @@ void run(int nsm) {
     long long cm = 0;
     for (auto x : c) cm = x > cm ? x : cm;
     const double floor_c = 256.0 * N / 512.0;
-    printf("2CTA M=256 N=%3d  err=%.2e (ref max %.1f)  cyc/mma=%.1f floor=%.0f eff=%.1f%%\n", N, err, mx,
+    printf("var%d 2CTA M=256 N=%3d  err=%.2e (ref max %.1f)  cyc/mma=%.1f floor=%.0f eff=%.1f%%\n", VAR, N, err, mx,
            (double)cm / iters, floor_c, 100.0 * floor_c * iters / cm);
     cudaFree(da); cudaFree(db); cudaFree(dd); cudaFree(dc);
 }
@@ -175,8 +170,8 @@ int main() {
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
     run<256>(nsm);
+    run<256, 1>(nsm);
+    run<256, 2>(nsm);
     run<128>(nsm);
-    run<64>(nsm);
-    run<32>(nsm);
     return 0;
 }
