@@ -2,32 +2,36 @@
 //
 // Hot path (reference: pnce/experiments.py:176-208 process_frames ->
 // pnce/estimator.py:68-86 correlate_rows):
-//   K1  k_lfsr / k_build_circulant : generate_mseq (pn.py:109-138) on device and
-//       the stacked lag-window rows A[j*L+l, k] = chip[(k - s_j - l) mod M]
-//       (estimator.py:62-65,114-117) as an fp16/bf16 K-major operand.
+//   K1  k_lfsr : generate_mseq (pn.py:109-138) on the device.
 //   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the
-//       received f32 (I,Q) samples into rows (frame, batch, rx, re|im) x K.
-//   K3  k_correlate : tcgen05 UMMA  D^T[rows, R] = B^T[rows, K] . A^T[K, R]
-//       (both real GEMMs of estimator.py:77-80 in one contraction; the huge
-//       frame x rx x re/im axis is the UMMA M dimension), TMA-fed, warp-specialised,
-//       persistent, TMEM double-buffered accumulator.
-//   K4  (fused into K3's epilogue) x 1/M, Re/Im pairing, per-transmitter window
-//       demux into taps[f, r, t, l] (experiments.py:206-207) and optional
-//       sum|e|, sum|e|^2, non-finite count vs. truth (metrics.py:19-25 + MSE).
+//       received f32 (I,Q) samples into 16-bit rows (frame, batch, rx, re|im) x K.
+//       Only used by the two-pass path; the fused K3 does this itself.
+//   K3  k_correlate : tcgen05 UMMA on a CTA pair (cta_group::2, M = 256 sample rows):
+//         D[rows, lags] = X[rows, K] . C[lags, K]^T
+//       where X are the CP-stripped samples (both real GEMMs of estimator.py:77-80 in
+//       one contraction: Re and Im are separate rows) and C[lag, k] = chip[(k - lag) mod M]
+//       are the stacked lag-window rows of batched_lag_rows (estimator.py:62-65,114-117).
+//       C is never materialised: every lag-window row block and every K step is a view
+//       into one resident "Hankel table" of 16-byte chip windows in shared memory (see
+//       DESIGN.md "circulant operand"), so the circulant costs no HBM/L2 traffic and no
+//       pipeline stage space.
+//   K4  fused into K3's epilogue: x 1/M, Re/Im pairing, per-transmitter window demux into
+//       taps[f, r, t, l] (experiments.py:206-207) and optional sum|e|, sum|e|^2 and
+//       non-finite count vs. truth (metrics.py:19-25 + the north-star MSE).
 #include <cuda.h>
-#include <cuda_fp16.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <atomic>
-#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <algorithm>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/pnce_b200.h"
@@ -37,10 +41,11 @@ using namespace pnce;
 
 namespace {
 
-constexpr int kBM = 128;       // UMMA M (input rows per tile)
+constexpr int kBM = 128;       // sample rows per CTA (UMMA M = 256 per pair)
 constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
 constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
 constexpr int kSmemLimit = 227 * 1024;
+constexpr uint32_t kStageA = kBM * kBK * 2;  // 16 KB A stage per CTA
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -50,55 +55,42 @@ pnce_status_t fail(pnce_status_t code, const std::string& msg) {
     return code;
 }
 
-#define CUDA_TRY(expr)                                                                 \
-    do {                                                                               \
-        cudaError_t e_ = (expr);                                                       \
-        if (e_ != cudaSuccess)                                                         \
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
             return fail(PNCE_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
     } while (0)
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
 
 // ------------------------------------------------------------------ K1: LFSR
 // One thread runs the Fibonacci LFSR for one period (pn.py:115-137):
 // out = MSB, fb = parity(state & tap_mask), state = ((state << 1) | fb) & mask.
-__global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m,
-                       int* period_out) {
+__global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m, int* period_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t mask = (1u << degree) - 1u;
     uint32_t s = state0;
     int n = 0;
     const int limit = 1 << degree;
     for (int i = 0; i < limit; ++i) {
-        uint32_t bit = (s >> (degree - 1)) & 1u;
+        const uint32_t bit = (s >> (degree - 1)) & 1u;
         if (n < m) chips[n] = bit ? -1.0f : 1.0f;
         ++n;
-        uint32_t fb = __popc(s & tap_mask) & 1u;
+        const uint32_t fb = __popc(s & tap_mask) & 1u;
         s = ((s << 1) | fb) & mask;
         if (s == state0) break;
     }
     *period_out = n;
 }
 
-// Stacked lag-window rows, K-major, zero padded: A[n, k] for n < rows_alloc, k < k_pad.
 template <typename T>
-__global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m,
-                                  int k_pad, int r_total, int rows_alloc, int l, int spacing, int repl) {
-    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)rows_alloc * k_pad * repl;
-    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-        int n = (int)((idx / k_pad) % rows_alloc);
-        int k = (int)(idx % k_pad);
-        float v = 0.0f;
-        if (n < r_total && k < m) {
-            int lag = (spacing * (n / l) + (n % l)) % m;  // shift_for_transmitter + window lag
-            int ci = k - lag;
-            if (ci < 0) ci += m;
-            v = chips[ci];
-        }
-        if constexpr (sizeof(T) == 2 && std::is_same<T, __half>::value)
-            a[idx] = __float2half_rn(v);
-        else
-            a[idx] = __float2bfloat16_rn(v);
-    }
+__device__ __forceinline__ T to16(float v) {
+    if constexpr (std::is_same<T, __half>::value) return __float2half_rn(v);
+    else return __float2bfloat16_rn(v);
 }
 
 // ------------------------------------------------------------------ K2: pack
@@ -106,65 +98,52 @@ __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict
 // row q (q = (f*nb + b)*n_r + r), write 8 quantised Re to packed row 2q and
 // 8 Im to row 2q+1 (16 B each); zero beyond M.
 template <typename T>
-__global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links,
-                          int samples, int c, int m, int k_pad) {
+__global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links, int samples, int c,
+                          int m, int k_pad) {
     const int chunks = k_pad >> 3;
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t total = n_links * chunks;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = idx / chunks;
-        const int ch = (int)(idx - q * chunks);
-        const int k0 = ch << 3;
+        const int k0 = (int)(idx - q * chunks) << 3;
         const float2* src = reinterpret_cast<const float2*>(iq) + q * samples + c + k0;
-        float re[8], im[8];
-        if (k0 + 8 <= m) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float2 v = __ldg(src + j);
-                re[j] = v.x;
-                im[j] = v.y;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
-                re[j] = v.x;
-                im[j] = v.y;
-            }
-        }
         uint4 pr, pi;
         T* hr = reinterpret_cast<T*>(&pr);
         T* hi = reinterpret_cast<T*>(&pi);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            if constexpr (std::is_same<T, __half>::value) {
-                hr[j] = __float2half_rn(re[j]);
-                hi[j] = __float2half_rn(im[j]);
-            } else {
-                hr[j] = __float2bfloat16_rn(re[j]);
-                hi[j] = __float2bfloat16_rn(im[j]);
-            }
+            const float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
+            hr[j] = to16<T>(v.x);
+            hi[j] = to16<T>(v.y);
         }
-        uint4* dst = reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0);
-        dst[0] = pr;
+        *reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0) = pr;
         *reinterpret_cast<uint4*>(out + (2 * q + 1) * (int64_t)k_pad + k0) = pi;
     }
 }
 
 // ------------------------------------------------------------------ K3+K4
-// Correlation kernel, one CTA pair (cluster 2x1, tcgen05 cta_group::2) per 256 input
-// rows.  Variants (template MODE):
-//   kModePacked   : rows = the packed 16-bit operand of K2, TMA-loaded;
-//   kModeFusedTma : rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
+// Variants (template MODE):
+//   kModePacked   : sample rows = the packed 16-bit operand of K2, TMA-loaded;
+//   kModeFusedTma : sample rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
 //                   converted (remove_cp + de-interleave + fp16/bf16) by converter warps
 //                   straight into the 128B-swizzled UMMA A stage -- K2 fused away;
-//   kModeFusedLdg : as above but converters LDG the f32 rows (fallback for row strides
-//                   that are not 16-byte multiples).
+//   kModeFusedLdg : as above, converters LDG the f32 rows (fallback for row strides that
+//                   are not 16-byte multiples).
 // Warp roles (16 warps, both CTAs unless noted):
-//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader) / arrive forwarder (peer)
-//   2 raw-row TMA producer (FusedTma)                3 spare
-//   4-7 converters (fused)                           8-15 epilogue (2 warps per TMEM lane quarter)
+//   0 TMA producer (packed rows)       1 MMA issuer (leader CTA)      2 raw-row TMA producer
+//   3 spare                            4-7 converters (fused)         8-15 epilogue
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
+constexpr int kWarps = 16;
+constexpr int kThreadsK3 = kWarps * 32;
+constexpr int kConvWarp0 = 4;
+constexpr int kConvWarps = 4;
+constexpr int kEpiWarp0 = 8;
+constexpr int kEpiWarps = 8;
+constexpr int kLinksPerTile = kBM / 2;                                          // 64 (re, im) row pairs
+constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
+constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
+constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;  // 64 links: 33 KB
+constexpr int kMaxUnitsPerGroup = 16;
 
 #ifdef PNCE_DIAG_TRACE
 // Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
@@ -175,48 +154,41 @@ __device__ __forceinline__ long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TRACE(slot, idx)                                                                   \
-    do {                                                                                   \
-        if (blockIdx.x < 2 && (idx) < kTraceMax)                                           \
-            g_trace[(blockIdx.x * kTraceSlots + (slot)) * kTraceMax + (idx)] = gtimer();  \
+#define TRACE(slot, idx)                                                                  \
+    do {                                                                                  \
+        if (blockIdx.x < 2 && (idx) < kTraceMax)                                          \
+            g_trace[(blockIdx.x * kTraceSlots + (slot)) * kTraceMax + (idx)] = gtimer(); \
     } while (0)
 #else
 #define TRACE(slot, idx) \
     do {                 \
     } while (0)
 #endif
-constexpr int kWarps = 16;
-constexpr int kThreadsK3 = kWarps * 32;
-constexpr int kConvWarp0 = 4;
-constexpr int kConvWarps = 4;
-constexpr int kEpiWarp0 = 8;
-constexpr int kEpiWarps = 8;
-constexpr int kLinksPerTile = kBM / 2;                                        // 64 (re, im) row pairs
-constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
-constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
-constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;         // 64 links: 33 KB
 
 struct CorrParams {
-    int64_t total_rows;  // n_frames * n_batches * n_r * 2
-    int32_t m_tiles;     // 256-row tiles (one per CTA pair)
-    int32_t n_groups;    // lag-row groups
-    int32_t g_cols;      // accumulator columns per group (= sum of the MMAs' N)
-    int32_t n_mma;       // MMAs per k-step (1 or 2), each N = nm
-    int32_t nm;
-    int32_t acc_stages;  // TMEM accumulator buffers (2 if 2*g_cols <= 512)
+    int64_t total_rows;   // n_frames * n_batches * n_r * 2
+    int32_t m_tiles;      // 256-row tiles (one per CTA pair)
+    int32_t n_groups;     // lag-unit groups per tile
+    int32_t units_per_group;
+    int32_t n_units;
+    int32_t nh;           // lag rows per CTA half of one unit (unit MMA N = 2*nh)
+    int32_t g_cols;       // accumulator columns per group = units_per_group * 2 * nh
+    int32_t acc_stages;   // TMEM accumulator buffers
     int32_t k_blocks;
-    int32_t stages;
-    int32_t raw_stages;  // FusedTma: f32 staging ring depth
-    int32_t circ_repl;   // circulant replicas
-    int32_t circ_rows;   // rows per replica
-    uint32_t stage_bytes;
-    uint32_t tx_bytes;   // transaction bytes per stage for BOTH CTAs of the pair
+    int32_t stages;       // A stages
+    int32_t raw_stages;   // FusedTma: f32 staging ring depth
+    int32_t table_rows;   // Hankel table rows (16 B each)
+    int32_t sigma;        // lag shift of the peer CTA's half == table shift of rank 1
+    uint32_t table_bytes; // 1024-aligned
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
     int32_t m, c, samples;  // PN length, CP length, samples per received row
     int32_t bf16;
     float inv_m;
+    const float* chips;     // device chips (K1 output)
+    const int32_t* unit_mu; // per unit: lag of B row 0 in the leader's half
+    const int2* chunk_map;  // per unit, per 8-column chunk: {R index of its first column, first valid col}
     const float* iq;
     float* taps;
     const float* truth;
@@ -233,8 +205,7 @@ __device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, in
     const int chunk = task & 7;
     const int64_t q = link0 + link_local;
     const int k0 = kb * kBK + chunk * 8;
-    const int64_t total_links = p.total_rows >> 1;
-    const bool ok = q < total_links;
+    const bool ok = q < (p.total_rows >> 1);
     const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -276,10 +247,11 @@ __device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask
 }
 
 // Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
-__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok,
-                                          int n_first, int n_valid, int64_t out_base, float& s_abs,
-                                          float& s_sq, float& s_bad) {
-    // Re/Im pairing: the even lane keeps columns 0..7, the odd lane columns 8..15.
+// The even lane owns accumulator columns 0..7 of the slice, the odd lane 8..15; the
+// 8 columns of an 8-chunk hold DEScending lags (Hankel order): column i <-> R index
+// rc0 - i, valid for i >= first_valid.
+__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok, int2 cm,
+                                          int n_valid, int64_t out_base, float& s_abs, float& s_sq, float& s_bad) {
     float x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -287,33 +259,37 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
     }
     if (!row_ok) return;
+    // o[2q], o[2q+1] = complex value for R index rc0 - 7 + q (ascending addresses)
     float o[16];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
-        o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
+    for (int q = 0; q < 8; ++q) {
+        const int i = 7 - q;
+        o[2 * q] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
+        o[2 * q + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
     }
-    if (p.stats != nullptr) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
-    }
-    const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
+    const int r_lo = cm.x - 7;                 // R index of o[0]
+    const int64_t g = out_base + r_lo;         // complex index of o[0]
+    const bool all = cm.y == 0 && cm.x < n_valid && r_lo >= 0;
 #ifdef PNCE_DIAG_NO_STORE
-    if (o[0] == 12345.678f) p.taps[g] = o[1];  // keep the work, drop the stores
+    if (o[0] == 12345.678f) p.taps[out_base] = o[1];  // keep the work, drop the stores
     return;
 #endif
-    if (n_first + 8 <= n_valid && (g & 3) == 0) {
+    if (all && (g & 3) == 0) {
         float* dst = p.taps + 2 * g;
         st_global_v8(dst, *reinterpret_cast<const float(*)[8]>(&o[0]));
         st_global_v8(dst + 8, *reinterpret_cast<const float(*)[8]>(&o[8]));
+        if (p.stats != nullptr) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (!(isfinite(o[2 * q]) && isfinite(o[2 * q + 1]))) s_bad += 1.f;
+        }
         if (p.truth != nullptr) {
             float h[16];
             ld_global_nc_v8(p.truth + 2 * g, *reinterpret_cast<float(*)[8]>(&h[0]));
             ld_global_nc_v8(p.truth + 2 * g + 8, *reinterpret_cast<float(*)[8]>(&h[8]));
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float dx = o[2 * i] - h[2 * i], dy = o[2 * i + 1] - h[2 * i + 1];
+            for (int q = 0; q < 8; ++q) {
+                const float dx = o[2 * q] - h[2 * q], dy = o[2 * q + 1] - h[2 * q + 1];
                 const float sq = dx * dx + dy * dy;
                 s_sq += sq;
                 s_abs += sqrtf(sq);
@@ -323,12 +299,14 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         float2* taps = reinterpret_cast<float2*>(p.taps);
         const float2* truth = reinterpret_cast<const float2*>(p.truth);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (n_first + i < n_valid) {
-                taps[g + i] = make_float2(o[2 * i], o[2 * i + 1]);
+        for (int q = 0; q < 8; ++q) {
+            const int r = r_lo + q;
+            if (7 - q >= cm.y && r >= 0 && r < n_valid) {
+                taps[g + q] = make_float2(o[2 * q], o[2 * q + 1]);
+                if (p.stats != nullptr && !(isfinite(o[2 * q]) && isfinite(o[2 * q + 1]))) s_bad += 1.f;
                 if (truth != nullptr) {
-                    const float2 h = __ldg(truth + g + i);
-                    const float dx = o[2 * i] - h.x, dy = o[2 * i + 1] - h.y;
+                    const float2 h = __ldg(truth + g + q);
+                    const float dx = o[2 * q] - h.x, dy = o[2 * q + 1] - h.y;
                     const float sq = dx * dx + dy * dy;
                     s_sq += sq;
                     s_abs += sqrtf(sq);
@@ -338,36 +316,54 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
     }
 }
 
+// CTA pair (cluster 2x1): the pair owns 256 sample rows (128 per CTA, UMMA M = 256,
+// cta_group::2); the leader CTA (rank 0) issues every MMA.  A lag "unit" is one MMA of
+// N = 2*nh lags: the leader's B half covers nh consecutive (descending) lags, the peer's
+// half the nh lags shifted by sigma -- both halves are views of the CTA's own Hankel
+// table (the peer's table is pre-shifted by sigma), so one descriptor serves both.
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
-k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
-            const CorrParams p) {
+k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
     constexpr bool FUSED = MODE != kModePacked;
     constexpr bool RAW = MODE == kModeFusedTma;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
-    // [A/B stages][1 KB barrier block][raw f32 stages]
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // [Hankel table][A stages][1 KB barrier block][raw f32 stages]
     const int S = p.stages;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+    uint8_t* table = smem;
+    uint8_t* a_base = smem + p.table_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(a_base + (size_t)S * kStageA);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint64_t* raw_full = tempty + 2;
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
-    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
+    uint8_t* raw_base = a_base + (size_t)S * kStageA + 1024;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
 
+    // ---- Hankel table: row rho (16 B) = chips[(rho + jj - rank*sigma) mod M], jj = 0..7
+    {
+        const int shift = (int)((p.m - (int)(((int64_t)rank * p.sigma) % p.m)) % p.m);
+        const int total = p.table_rows * 8;
+        for (int idx = threadIdx.x; idx < total; idx += kThreadsK3) {
+            int ci = (idx >> 3) + (idx & 7) + shift;
+            ci %= p.m;
+            const float v = __ldg(p.chips + ci);
+            if (p.bf16) reinterpret_cast<__nv_bfloat16*>(table)[idx] = __float2bfloat16_rn(v);
+            else reinterpret_cast<__half*>(table)[idx] = __float2half_rn(v);
+        }
+        fence_proxy_async_smem();
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
-            // bytes and converter arrives land on the leader's barrier).
-            mbar_init(&full[s], FUSED ? 1 + 2 * kConvWarps : 1);
+            // Leader: (packed) the producer's expect_tx arrive; (fused) the converter warps
+            // of BOTH CTAs -- the peer's TMA bytes and converter arrives land here too.
+            mbar_init(&full[s], FUSED ? 2 * kConvWarps : 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -382,10 +378,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         }
         fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) {
-        if (!FUSED || RAW) tma_prefetch(&tm_in);
-        tma_prefetch(&tm_circ);
-    }
+    if (warp == 0 && lane == 0 && MODE != kModeFusedLdg) tma_prefetch(&tm_in);
     if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
     tc_fence_before();
     cluster_sync_all();
@@ -397,41 +390,37 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int total_tiles = p.m_tiles * p.n_groups;
     const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
-    const uint32_t a_bytes = kBM * kBK * 2;
-    const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
+        if (!FUSED && lane == 0) {
+            // ===== TMA producer: packed sample rows; bytes land on the leader's barrier
             const uint64_t pol_in = policy_evict_first();
-            const uint64_t pol_circ = policy_evict_last();
-            const int circ_row0 = (cid % p.circ_repl) * p.circ_rows;
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
-                const int tile = cid + ti * n_clusters;
-                const int mt = tile / p.n_groups;
-                const int g = tile - mt * p.n_groups;
+                const int mt = (cid + ti * n_clusters) / p.n_groups;
                 const int stage = j % S;
                 mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
                 TRACE(0, j);
-                uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
-                uint8_t* sb = sa + a_bytes;
-                const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
-                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-                if (!FUSED)
-                    tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
-                for (int jj = 0; jj < p.n_mma; ++jj)
-                    tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
-                                     circ_row0 + g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
+                if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageA);
+                tma_load_2d_pair(a_base + (size_t)stage * kStageA, &tm_in, mapa_shared(smem_u32(&full[stage]), 0),
+                                 kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
             }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
+            const uint32_t tbl = smem_u32(table);
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int ti = 0; ti < my_tiles; ++ti) {
+                const int g = (cid + ti * n_clusters) % p.n_groups;
+                const int u0 = g * p.units_per_group;
+                const int nu = min(p.units_per_group, p.n_units - u0);
+                int rho[kMaxUnitsPerGroup];  // Hankel start row per unit, advanced by 16 per k-step
+#pragma unroll
+                for (int u = 0; u < kMaxUnitsPerGroup; ++u)
+                    if (u < nu) rho[u] = (p.m - __ldg(p.unit_mu + u0 + u) % p.m) % p.m;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 TRACE(1, ti);
                 tc_fence_after();
@@ -439,22 +428,23 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const int j = ti * p.k_blocks + kb;
                     const int stage = j % S;
-                    const uint32_t phase = (uint32_t)(j / S) & 1u;
 #ifndef PNCE_DIAG_NO_FULLWAIT
-                    mbar_wait(&full[stage], phase);
-#else
-                    (void)phase;
+                    mbar_wait(&full[stage], (uint32_t)(j / S) & 1u);
 #endif
                     TRACE(2, j);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-                    const uint32_t sb = sa + a_bytes;
+                    const uint32_t sa = smem_u32(a_base + (size_t)stage * kStageA);
 #pragma unroll
                     for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
-                        for (int jj = 0; jj < p.n_mma; ++jj) {
-                            const uint64_t bd = make_sdesc(sb + jj * b_half_bytes + ks * 32, 16, 1024, 2);
-                            umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
+#pragma unroll
+                        for (int u = 0; u < kMaxUnitsPerGroup; ++u) {
+                            if (u < nu) {
+                                const uint64_t bd = make_sdesc(tbl + (uint32_t)rho[u] * 16u, 128, 128, 0);
+                                umma_f16_ss_pair(d_tmem + (uint32_t)(u * 2 * p.nh), ad, bd, p.idesc, (kb | ks) != 0);
+                                rho[u] += kUmmaK;
+                                if (rho[u] >= p.m) rho[u] -= p.m;
+                            }
                         }
                     }
                     umma_commit_pair(&empty[stage]);
@@ -467,7 +457,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     } else if (warp == 2) {
         if (RAW && lane == 0) {
             // ===== raw-row producer: TMA the f32 (I,Q) rows of this CTA's 64 links for one
-            // K-block (64 links x 64 samples x 8 B = 32 KB) into the staging ring.
+            // K-block (64 links x 64 samples x 8 B + slack) into the staging ring.
             const uint64_t pol = policy_evict_first();
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
@@ -482,23 +472,24 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #else
                 mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
                 // box start rounded down to a 16-byte boundary; converters skip the slack
-                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs],
-                            (2 * (p.c + kb * kBK)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile, pol);
+                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs], (2 * (p.c + kb * kBK)) & ~3,
+                            (mt * 2 + (int)rank) * kLinksPerTile, pol);
 #endif
             }
         }
     } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
         if (FUSED) {
             const int cw = warp - kConvWarp0;
+            const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
                 const int stage = j % S;
-                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                const uint32_t sa = smem_u32(a_base + (size_t)stage * kStageA);
                 if (RAW) {
                     // staged f32 rows -> A stage.  Warp w converts links w, w+4, ...; lane l
-                    // handles samples 2l, 2l+1 (one conflict-free LDS.128 of the 512 B row,
-                    // two STS.32 into the Re / Im rows).
+                    // handles samples 2l, 2l+1 (one conflict-free LDS of the staged row, two
+                    // STS.32 into the Re / Im rows).
                     const int rs = j % p.raw_stages;
                     mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
                     if (cw == 0 && lane == 0) TRACE(7, j);
@@ -512,12 +503,13 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #pragma unroll 4
                     for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
                         const int link_local = cw + kConvWarps * i;
+                        const uint32_t src = raw + link_local * (kRawRowFloats * 4);
                         float4 v;
                         if (slack == 0) {
-                            v = ld_shared_v4f(raw + link_local * (kRawRowFloats * 4));
+                            v = ld_shared_v4f(src);
                         } else {
-                            const float2 a = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4));
-                            const float2 b = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4) + 8);
+                            const float2 a = ld_shared_v2f(src);
+                            const float2 b = ld_shared_v2f(src + 8);
                             v = make_float4(a.x, a.y, b.x, b.y);
                         }
                         if (!ok0) { v.x = 0.f; v.y = 0.f; }
@@ -531,9 +523,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        // proxy fence above completed this warp's STS; plain (CTA-scope
-                        // release) arrive on the leader's barrier, no GPU-scope membar
-                        mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                        // the proxy fence completed this warp's STS; plain (CTA-scope release)
+                        // arrive on the leader's barrier, no GPU-scope membar
+                        mbar_arrive_remote(full_leader0 + (uint32_t)(stage * 8));
                         mbar_arrive(&raw_empty[rs]);
                         if (cw == 0) TRACE(9, j);
                     }
@@ -544,14 +536,13 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     const int ct = cw * 32 + lane;
                     ConvTask buf[kTasksPerThread];
 #pragma unroll
-                    for (int i = 0; i < kTasksPerThread; ++i)
-                        conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
+                    for (int i = 0; i < kTasksPerThread; ++i) conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
                     mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
 #pragma unroll
                     for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                    if (lane == 0) mbar_arrive_remote(full_leader0 + (uint32_t)(stage * 8));
                 }
             }
         }
@@ -563,6 +554,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         const int c_begin = min(p.g_cols, half * cph);
         const int c_end = min(p.g_cols, c_begin + cph);
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const int chunks_per_unit = (2 * p.nh) / 8;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int ti = 0; ti < my_tiles; ++ti) {
@@ -584,10 +576,15 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
             const int n_valid = n_tx * p.l;
             const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
+            const int2* cmap = p.chunk_map + (size_t)g * p.units_per_group * chunks_per_unit;
+            const int n_map = min(p.units_per_group, p.n_units - g * p.units_per_group) * chunks_per_unit;
             float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
+            auto chunk_of = [&](int col) -> int2 {
+                const int ci = (col >> 3) + (odd ? 1 : 0);
+                return ci < n_map ? __ldg(cmap + ci) : make_int2(0, 8);
+            };
 
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.g_cols);
-            const int n_tile0 = g * p.g_cols;
             // 32-column chunks (two 16-column slices each); the next chunk's TMEM load is
             // in flight while the current one is paired, scaled and stored.
             uint32_t va[32], vb[32];
@@ -598,17 +595,15 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 while (true) {
                     const bool more = c0 + 64 <= c_end;
                     if (more) tmem_ld32_nowait(t_row + c0 + 32, vb);
-                    epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, va + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
-                              s_sq, s_bad);
+                    epi_slice(p, va, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va + 16, odd, row_ok, chunk_of(c0 + 16), n_valid, out_base, s_abs, s_sq, s_bad);
                     c0 += 32;
                     if (!more) break;
                     tmem_wait_ld();
                     const bool more2 = c0 + 64 <= c_end;
                     if (more2) tmem_ld32_nowait(t_row + c0 + 32, va);
-                    epi_slice(p, vb, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, vb + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
-                              s_sq, s_bad);
+                    epi_slice(p, vb, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb + 16, odd, row_ok, chunk_of(c0 + 16), n_valid, out_base, s_abs, s_sq, s_bad);
                     c0 += 32;
                     if (!more2) break;
                     tmem_wait_ld();
@@ -617,14 +612,13 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (c0 < c_end) {  // 16-column remainder
                 tmem_ld16_nowait(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(va));
                 tmem_wait_ld();
-                epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                epi_slice(p, va, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
             }
             // this warp's share of the accumulator is drained -> tell the leader's MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
             if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
-            if (lane == 0 && warp == kEpiWarp0 + kEpiWarps - 1) TRACE(12, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
 
             if (p.stats != nullptr) {
@@ -674,27 +668,24 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     std::call_once(once, [] {
         void* ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-                cudaSuccess &&
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     });
     return fn;
 }
 
-// 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128B swizzle.
-pnce_status_t make_tmap(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
-                        uint32_t box_rows, int bf16) {
+// Packed sample rows: 2-D [rows][k_pad] 16-bit, box [128 rows][64], 128B swizzle.
+pnce_status_t make_tmap_packed(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, int bf16) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                     2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return PNCE_OK;
 }
@@ -716,60 +707,108 @@ pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_fl
     return PNCE_OK;
 }
 
-}  // namespace
-
-// Lag-row tiling of one K3 variant.
-struct Tiling {
-    int n_groups;    // lag-row groups per 256-row tile
-    int g_cols;      // accumulator columns per group
-    int n_mma;       // pair MMAs per k-step (N = nm each)
-    int nm;
-    int acc_stages;  // TMEM accumulator buffers
-    int stages;      // smem pipeline depth
-    uint32_t stage_bytes;
-    uint32_t tmem_cols;
-    CUtensorMap tm_circ;  // circulant rows, box = nm/2 rows x 64 K
+// Lag layout: which lag rows each MMA "unit" covers and where each accumulator column
+// lands in the taps.
+struct LagLayout {
+    int nh = 8;                 // rows per CTA half (multiple of 8, <= 128)
+    int sigma = 0;              // lag shift of the peer half (Hankel table shift of rank 1)
+    std::vector<int32_t> mu;    // per unit: lag of B row 0 of the leader's half
+    std::vector<int2> chunks;   // per unit, per 8-column chunk: {R index of column 0, first valid column}
 };
+
+LagLayout plan_lags(const pnce_cfg_t& c) {
+    LagLayout L;
+    const int M = c.m, Lw = c.l, Nb = c.n_batch;
+    const int delta = M / Nb;
+    auto r8 = [](int x) { return (x + 7) / 8 * 8; };
+    const bool pair_mode = Lw <= 128 && Nb >= 2 && delta > Lw;
+    if (pair_mode) {
+        // unit u = windows (2u, 2u+1): the peer half is the next window, sigma = delta
+        L.nh = r8(Lw);
+        L.sigma = delta;
+        const int units = (Nb + 1) / 2;
+        for (int u = 0; u < units; ++u) {
+            L.mu.push_back(2 * u * delta + L.nh - 1);
+            for (int h = 0; h < 2; ++h) {
+                const int j = 2 * u + h;
+                for (int q = 0; q < L.nh / 8; ++q) {
+                    const int l0 = L.nh - 1 - 8 * q;  // tap of column 0 of this chunk (descending)
+                    int first_valid = std::max(0, std::min(8, l0 - Lw + 1));
+                    if (j >= Nb) first_valid = 8;
+                    L.chunks.push_back(make_int2(j * Lw + l0, first_valid));
+                }
+            }
+        }
+        return L;
+    }
+    // chunk mode: windows split into units of 2*nh contiguous lags (peer = next nh lags)
+    struct Window { int start, len, r_off; };
+    std::vector<Window> wins;
+    if (delta == Lw || Nb == 1) wins.push_back({0, Nb * Lw, 0});  // one contiguous lag range
+    else
+        for (int j = 0; j < Nb; ++j) wins.push_back({j * delta, Lw, j * Lw});
+    const int maxlen = wins[0].len;
+    L.nh = std::min(128, r8((maxlen + 1) / 2));
+    L.sigma = L.nh;
+    for (const Window& w : wins) {
+        const int units = (w.len + 2 * L.nh - 1) / (2 * L.nh);
+        for (int u = 0; u < units; ++u) {
+            const int base = 2 * L.nh * u;
+            L.mu.push_back(w.start + base + L.nh - 1);
+            for (int h = 0; h < 2; ++h)
+                for (int q = 0; q < L.nh / 8; ++q) {
+                    const int l0 = base + h * L.nh + L.nh - 1 - 8 * q;
+                    const int first_valid = std::max(0, std::min(8, l0 - w.len + 1));
+                    L.chunks.push_back(make_int2(w.r_off + l0, first_valid));
+                }
+        }
+    }
+    return L;
+}
+
+// Unit grouping for one K3 variant.
+struct Tiling {
+    int units_per_group;
+    int n_groups;
+    int g_cols;
+    int acc_stages;
+    uint32_t tmem_cols;
+};
+
+Tiling make_tiling(int n_units, int nh, int max_cols) {
+    Tiling t{};
+    const int unit_cols = 2 * nh;
+    int per = std::max(1, std::min(std::min(n_units, kMaxUnitsPerGroup), max_cols / unit_cols));
+    t.n_groups = (n_units + per - 1) / per;
+    t.units_per_group = (n_units + t.n_groups - 1) / t.n_groups;
+    t.g_cols = t.units_per_group * unit_cols;
+    t.acc_stages = (2 * t.g_cols <= 512) ? 2 : 1;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(t.acc_stages * t.g_cols)) cols <<= 1;
+    t.tmem_cols = cols;
+    return t;
+}
+
+}  // namespace
 
 struct pnce_plan {
     pnce_cfg_t cfg;
     int n_batches;
-    int r_total;     // N_b * L
-    int k_pad;       // roundup(M, 64)
-    int rows_alloc;  // circulant rows per replica (>= both tilings' coverage)
-    int repl;        // circulant replicas: CTA pairs spread their B loads over replicas so
-                     // the whole grid does not hammer the same L2 lines in lock-step
+    int k_pad;        // roundup(M, 64)
     int num_sms;
-    Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
-    Tiling packed;   // packed operand in: groups of <= 256 cols, double-buffered accumulator
-    float* chips;    // device [m]
-    void* circ;      // device [rows_alloc][k_pad] 16-bit
+    LagLayout lags;
+    Tiling fused;     // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
+    Tiling packed;    // packed operand in: groups of <= 256 cols, double-buffered accumulator
+    int table_rows;
+    uint32_t table_bytes;
+    float* chips;         // device [m]
+    int32_t* unit_mu;     // device [n_units]
+    int2* chunk_map;      // device [n_units * 2nh/8]
 };
-
-static void make_tiling(Tiling& t, int r_total, int max_group) {
-    const int r16 = (r_total + 15) / 16 * 16;
-    t.n_groups = (r16 + max_group - 1) / max_group;
-    int g = ((r16 + t.n_groups - 1) / t.n_groups + 15) / 16 * 16;
-    if (g > 256) {
-        g = (g + 31) / 32 * 32;
-        t.n_mma = 2;
-    } else {
-        t.n_mma = 1;
-    }
-    t.g_cols = g;
-    t.nm = g / t.n_mma;
-    t.acc_stages = (2 * g <= 512) ? 2 : 1;
-    t.stage_bytes = (uint32_t)(kBM * kBK * 2 + (g / 2) * kBK * 2);
-    int stages = (int)((kSmemLimit - 2048) / t.stage_bytes);
-    t.stages = stages > 8 ? 8 : stages;
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(t.acc_stages * g)) cols <<= 1;
-    t.tmem_cols = cols;
-}
 
 extern "C" {
 
-int32_t pnce_version(void) { return 100; }
+int32_t pnce_version(void) { return 200; }
 
 const char* pnce_last_error(void) { return g_err.c_str(); }
 
@@ -777,16 +816,13 @@ int64_t pnce_kernel_launches(void) { return g_launches.load(); }
 
 pnce_status_t pnce_config_check(const pnce_cfg_t* cfg) {
     if (!cfg) return fail(PNCE_ERR_INVALID_CONFIG, "null config");
-    if (cfg->degree < 2 || cfg->degree > 16)
-        return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
+    if (cfg->degree < 2 || cfg->degree > 16) return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
     const uint32_t full = (1u << cfg->degree) - 1u;
     if (cfg->state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
     if (cfg->state > full) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
-    if (!(cfg->tap_mask & (1u << (cfg->degree - 1))))
-        return fail(PNCE_ERR_INVALID_SPEC, "tap set must include the degree");
+    if (!(cfg->tap_mask & (1u << (cfg->degree - 1)))) return fail(PNCE_ERR_INVALID_SPEC, "tap set must include the degree");
     if (cfg->tap_mask & ~full) return fail(PNCE_ERR_INVALID_SPEC, "tap outside [1, degree]");
-    if ((int64_t)cfg->m != (int64_t)full)
-        return fail(PNCE_ERR_INVALID_CONFIG, "m must equal 2^degree - 1");
+    if ((int64_t)cfg->m != (int64_t)full) return fail(PNCE_ERR_INVALID_CONFIG, "m must equal 2^degree - 1");
     if (cfg->n_t < 1 || cfg->n_r < 1) return fail(PNCE_ERR_INVALID_CONFIG, "n_t, n_r must be >= 1");
     if (!(1 <= cfg->l && cfg->l <= cfg->c && cfg->c <= cfg->m))
         return fail(PNCE_ERR_INVALID_CONFIG, "need 1 <= L <= C <= M");
@@ -805,8 +841,8 @@ pnce_status_t pnce_config_check(const pnce_cfg_t* cfg) {
     return PNCE_OK;
 }
 
-pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state, float* chips_dev,
-                                 int32_t m, void* stream) {
+pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state, float* chips_dev, int32_t m,
+                                 void* stream) {
     if (degree < 2 || degree > 16) return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
     if (state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
     if (state >= (1u << degree)) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
@@ -823,8 +859,8 @@ pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t sta
     cudaFreeAsync(d_period, st);
     if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("k_lfsr: ") + cudaGetErrorString(e));
     if (period != m)
-        return fail(PNCE_ERR_NOT_MAXIMAL, "LFSR period " + std::to_string(period) + " != " +
-                                              std::to_string(m) + "; feedback polynomial is not primitive");
+        return fail(PNCE_ERR_NOT_MAXIMAL, "LFSR period " + std::to_string(period) + " != " + std::to_string(m) +
+                                              "; feedback polynomial is not primitive");
     return PNCE_OK;
 }
 
@@ -843,21 +879,24 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     pnce_plan* p = new pnce_plan();
     p->cfg = *cfg;
     p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
-    p->r_total = cfg->n_batch * cfg->l;
     p->k_pad = (cfg->m + kBK - 1) / kBK * kBK;
-    // Tuning knobs (diagnostics): maximum accumulator columns per lag-row group.
-    const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
-    const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
-    make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
-    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 256);
-    p->rows_alloc = std::max(p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols);
     p->num_sms = sms;
+    p->lags = plan_lags(*cfg);
+    const int n_units = (int)p->lags.mu.size();
+    p->fused = make_tiling(n_units, p->lags.nh, env_int("PNCE_TUNE_GROUP_FUSED", 512));
+    p->packed = make_tiling(n_units, p->lags.nh, env_int("PNCE_TUNE_GROUP_PACKED", 256));
+    p->table_rows = (cfg->m + p->lags.nh + 2 * kUmmaK + 7) / 8 * 8;
+    p->table_bytes = (uint32_t)((p->table_rows * 16 + 1023) / 1024 * 1024);
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    const char* rp = std::getenv("PNCE_TUNE_CIRC_REPL");
-    p->repl = std::max(1, std::min(64, rp ? std::atoi(rp) : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2 * p->repl);
+    if (e == cudaSuccess) e = cudaMalloc(&p->unit_mu, sizeof(int32_t) * n_units);
+    if (e == cudaSuccess) e = cudaMalloc(&p->chunk_map, sizeof(int2) * p->lags.chunks.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->unit_mu, p->lags.mu.data(), sizeof(int32_t) * n_units, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(p->chunk_map, p->lags.chunks.data(), sizeof(int2) * p->lags.chunks.size(),
+                            cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
@@ -867,36 +906,10 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         pnce_plan_destroy(p);
         return s;
     }
-    const int spacing = cfg->m / cfg->n_batch;
-    const int64_t total = (int64_t)p->rows_alloc * p->k_pad * p->repl;
-    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    if (cfg->dtype == PNCE_DTYPE_BF16)
-        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
-    else
-        k_build_circulant<__half><<<blocks, 256, 0, st>>>(
-            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
-    g_launches++;
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-        pnce_plan_destroy(p);
-        return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
-    }
-    const uint64_t circ_rows = (uint64_t)p->rows_alloc * p->repl;
-    s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
-    if (s == PNCE_OK)
-        s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
-                      cfg->dtype == PNCE_DTYPE_BF16);
-    if (s != PNCE_OK) {
-        pnce_plan_destroy(p);
-        return s;
-    }
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(k_correlate<kModePacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kSmemLimit);
+        attr_err = cudaFuncSetAttribute(k_correlate<kModePacked>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
         if (attr_err == cudaSuccess)
             attr_err = cudaFuncSetAttribute(k_correlate<kModeFusedLdg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmemLimit);
@@ -915,7 +928,8 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
 pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
     if (!p) return PNCE_OK;
     if (p->chips) cudaFree(p->chips);
-    if (p->circ) cudaFree(p->circ);
+    if (p->unit_mu) cudaFree(p->unit_mu);
+    if (p->chunk_map) cudaFree(p->chunk_map);
     delete p;
     return PNCE_OK;
 }
@@ -933,8 +947,7 @@ size_t pnce_workspace_bytes(const pnce_plan_t* p, int64_t n_frames) {
     return (size_t)rows * p->k_pad * 2;
 }
 
-pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, int64_t n_frames,
-                           void* stream) {
+pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, int64_t n_frames, void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
@@ -946,7 +959,7 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
     const int64_t work = links * (p->k_pad / 8);
     const int64_t want = (work + 255) / 256;
-    const int blocks = (int)(want < (int64_t)p->num_sms * 16 ? want : (int64_t)p->num_sms * 16);
+    const int blocks = (int)std::min<int64_t>(want, (int64_t)p->num_sms * 16);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (c.dtype == PNCE_DTYPE_BF16)
         k_pack_iq<__nv_bfloat16><<<blocks, 256, 0, st>>>(iq, (__nv_bfloat16*)packed, links, samples, c.c, c.m, p->k_pad);
@@ -957,9 +970,13 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     return PNCE_OK;
 }
 
-// Shared launch setup for both K3 variants.
-static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fused, float* taps, const float* truth,
-                                 double* stats, int64_t n_frames, CorrParams& prm) {
+}  // extern "C"
+
+namespace {
+
+// Shared launch setup for all K3 variants.
+pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, float* taps, const float* truth, double* stats,
+                          int64_t n_frames, CorrParams& prm) {
     if ((reinterpret_cast<uintptr_t>(taps) & 7) || (truth && (reinterpret_cast<uintptr_t>(truth) & 7)))
         return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
     const pnce_cfg_t& c = p->cfg;
@@ -969,19 +986,17 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     if (m_tiles * t.n_groups > INT32_MAX || prm.total_rows > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
-    prm.circ_repl = p->repl;
-    prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
+    prm.units_per_group = t.units_per_group;
+    prm.n_units = (int)p->lags.mu.size();
+    prm.nh = p->lags.nh;
     prm.g_cols = t.g_cols;
-    prm.n_mma = t.n_mma;
-    prm.nm = t.nm;
     prm.acc_stages = t.acc_stages;
     prm.k_blocks = p->k_pad / kBK;
-    prm.stages = t.stages;
-    prm.stage_bytes = t.stage_bytes;
-    const uint32_t b_half = (uint32_t)(t.g_cols / 2) * kBK * 2;
-    prm.tx_bytes = 2 * (b_half + (fused ? 0u : (uint32_t)(kBM * kBK * 2)));
-    prm.idesc = make_idesc_f16(2 * kBM, t.nm, c.dtype == PNCE_DTYPE_BF16);
+    prm.table_rows = p->table_rows;
+    prm.table_bytes = p->table_bytes;
+    prm.sigma = p->lags.sigma;
+    prm.idesc = make_idesc_f16(2 * kBM, 2 * p->lags.nh, c.dtype == PNCE_DTYPE_BF16);
     prm.tmem_cols = t.tmem_cols;
     prm.n_r = c.n_r;
     prm.n_t = c.n_t;
@@ -993,34 +1008,47 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.samples = c.c + c.m + c.l - 1;
     prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
     prm.inv_m = 1.0f / (float)c.m;
+    prm.chips = p->chips;
+    prm.unit_mu = p->unit_mu;
+    prm.chunk_map = p->chunk_map;
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
     return PNCE_OK;
 }
 
-static int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
+int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
     const int64_t tiles = (int64_t)prm.m_tiles * prm.n_groups;
     const int64_t pairs = std::min<int64_t>(tiles, p->num_sms / 2);
     return (int)(2 * std::max<int64_t>(pairs, 1));
 }
 
-pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
-                             double* stats, int64_t n_frames, void* stream) {
+size_t smem_budget(const CorrParams& prm) {
+    return 1024 + prm.table_bytes + (size_t)prm.stages * kStageA + 1024 + (size_t)prm.raw_stages * kRawStageBytes;
+}
+
+}  // namespace
+
+extern "C" {
+
+pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth, double* stats,
+                             int64_t n_frames, void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
     if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->packed, false, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, p->packed, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     CUtensorMap tm_in;
-    s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
+    s = make_tmap_packed(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, p->cfg.dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) return s;
-    const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, static_cast<cudaStream_t>(stream)>>>(
-        tm_in, p->packed.tm_circ, prm);
+    const int64_t avail = (int64_t)kSmemLimit - 2048 - prm.table_bytes;
+    prm.stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_AB_STAGES", 12), avail / kStageA);
+    if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the correlator pipeline");
+    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), static_cast<cudaStream_t>(stream)>>>(
+        tm_in, prm);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;
@@ -1037,30 +1065,27 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->fused, true, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, p->fused, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
-    const int samples = prm.samples;
-    const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
-    bool raw_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
-    if (fm && std::atoi(fm) == kModeFusedLdg) raw_ok = false;
+    const int64_t avail = (int64_t)kSmemLimit - 2048 - prm.table_bytes;
+    bool raw_ok = ((size_t)prm.samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
+    if (env_int("PNCE_TUNE_FUSED_MODE", kModeFusedTma) == kModeFusedLdg) raw_ok = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (raw_ok) {
-        // f32 rows TMA-staged in shared memory (default): raw ring + A/B ring
-        const char* rs = std::getenv("PNCE_TUNE_RAW_STAGES");
-        prm.raw_stages = rs ? std::max(1, std::atoi(rs)) : 2;
-        const int64_t avail = (int64_t)kSmemLimit - 2048 - (int64_t)prm.raw_stages * kRawStageBytes;
-        int ab = (int)std::min<int64_t>(8, avail / (int64_t)prm.stage_bytes);
-        const char* as = std::getenv("PNCE_TUNE_AB_STAGES");
-        if (as) ab = std::min(ab, std::max(1, std::atoi(as)));
-        if (ab < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
-        prm.stages = ab;
+        // f32 rows TMA-staged in shared memory (default): raw ring + A ring
+        prm.stages = std::max(2, env_int("PNCE_TUNE_AB_STAGES", 4));
+        prm.raw_stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_RAW_STAGES", 6),
+                                                (avail - (int64_t)prm.stages * kStageA) / kRawStageBytes);
+        if (prm.raw_stages < 2) {
+            prm.stages = 2;
+            prm.raw_stages = (int)std::min<int64_t>(6, (avail - 2 * (int64_t)kStageA) / kRawStageBytes);
+        }
+        if (prm.raw_stages < 1) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         CUtensorMap tm_raw;
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)(prm.total_rows / 2));
+        s = make_tmap_raw(&tm_raw, iq, (uint64_t)prm.samples * 2, (uint64_t)(prm.total_rows / 2));
         if (s != PNCE_OK) return s;
-        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
-                            (size_t)prm.raw_stages * kRawStageBytes;
-        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
+        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(tm_raw, prm);
 #ifdef PNCE_DIAG_TRACE
         if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
             static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
@@ -1073,10 +1098,11 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         }
 #endif
     } else {
-        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        // tm_in is unused by the LDG-fused variant; pass the circulant map in its slot.
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(p->fused.tm_circ,
-                                                                                   p->fused.tm_circ, prm);
+        prm.stages = (int)std::min<int64_t>(12, avail / kStageA);
+        if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        CUtensorMap dummy;
+        std::memset(&dummy, 0, sizeof(dummy));
+        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(dummy, prm);
     }
     g_launches++;
     CUDA_TRY(cudaGetLastError());

@@ -287,3 +287,32 @@ def test_packed_path_matches_fused(dev):
     fused, _ = corr.process(x)
     packed, _ = corr.correlate(corr.pack(x), 1)
     assert torch.equal(fused, packed)
+
+
+# Lag-layout coverage of the resident Hankel-table circulant: window pairs (odd/even N_b,
+# L not a multiple of 8), chunked long windows (L > 128), a single window, and the
+# contiguous-lag case (delta == L).
+LAYOUTS = [
+    # (n_t, n_r, m, l, c, n_batch)
+    (5, 3, 255, 20, 20, 5),      # pair mode, odd N_b, L % 8 != 0
+    (6, 4, 511, 64, 64, 3),      # pair mode, odd N_b
+    (4, 2, 1023, 200, 200, 2),   # chunk mode, separate windows, L > 128
+    (3, 2, 511, 128, 128, 1),    # single window
+    (4, 2, 127, 8, 8, 4),        # pair mode, tiny windows
+    (16, 2, 1023, 127, 127, 8),  # contiguous lags (delta == L)
+    (8, 2, 2047, 256, 256, 7),   # chunk mode, several long windows
+]
+
+
+@pytest.mark.parametrize("n_t,n_r,m,l,c,nb", LAYOUTS)
+def test_lag_layouts(dev, n_t, n_r, m, l, c, nb):
+    cfg, ocfg = make_cfg(n_t, m, l, nb, n_r=n_r, c=c)
+    chips, iq, _ = sim_sets(ocfg, 2)
+    deg = (m + 1).bit_length() - 1
+    corr = P.Correlator(P.default_spec(deg), cfg, n_r, device=dev)
+    x = torch.from_numpy(iq).to(dev)
+    taps, _ = corr.process(x)
+    ref = oracle_est(chips, ocfg, iq)
+    assert link_err(taps.cpu().numpy(), ref) <= TOL
+    packed, _ = corr.correlate(corr.pack(x), 2)
+    assert torch.equal(taps, packed)

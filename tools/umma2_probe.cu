@@ -85,7 +85,19 @@ k_probe2(const __half* __restrict__ a_full, const __half* __restrict__ b_full, i
             if (VAR == 1) { ks = (it >> 1) & 3; dcol = (it & 1) * 256; }          // alternate accumulators
             if (VAR == 2) { ks = it & 3; dcol = ((it >> 2) & 1) * 256; }          // 4 then switch
             const uint64_t ad = make_sdesc(smem_u32(sA) + ks * 32, 16, 1024, 2);
-            const uint64_t bd = make_sdesc(smem_u32(sB) + ks * 32, 16, 1024, 2);
+            uint64_t bd = make_sdesc(smem_u32(sB) + ks * 32, 16, 1024, 2);
+            if (VAR == 3) bd = make_sdesc(smem_u32(sB) + ((it * 16) % 1024) * 16 % 8192, 128, 128, 0);
+            if (VAR == 4) bd = make_sdesc(smem_u32(sB) + ks * 256, 128, 256, 0);
+            if (VAR == 5) bd = make_sdesc(smem_u32(sB) + ((it * 16 + 3) % 256) * 16, 128, 128, 0);
+            if (VAR == 6) {  // kernel pattern: 4 units (mu = 63 + 254u), k-step s = it / 4
+                const int u = it & 3, st = it >> 2;
+                const int rho = ((16 * st - (63 + 254 * u)) % 1023 + 1023) % 1023;
+                bd = make_sdesc(smem_u32(sB) + (rho % 960) * 16, 128, 128, 0);
+            }
+            if (VAR == 7) {  // 4 units, same start (no jumps)
+                const int st = it >> 2;
+                bd = make_sdesc(smem_u32(sB) + ((16 * st) % 960) * 16, 128, 128, 0);
+            }
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
@@ -169,9 +181,9 @@ void run(int nsm) {
 int main() {
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    run<256>(nsm);
-    run<256, 1>(nsm);
-    run<256, 2>(nsm);
-    run<128>(nsm);
+    run<128, 3>(nsm);
+    run<128, 6>(nsm);
+    run<128, 7>(nsm);
+    run<256, 6>(nsm);
     return 0;
 }
