@@ -2,19 +2,18 @@
 //
 // Hot path (reference: pnce/experiments.py:176-208 process_frames ->
 // pnce/estimator.py:68-86 correlate_rows):
-//   K1  k_lfsr : generate_mseq (pn.py:109-138) on the device.
-//   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the
-//       received f32 (I,Q) samples into 16-bit rows (frame, batch, rx, re|im) x K.
-//       Only used by the two-pass path; the fused K3 does this itself.
-//   K3  k_correlate : tcgen05 UMMA on a CTA pair (cta_group::2, M = 256 sample rows):
-//         D[rows, lags] = X[rows, K] . C[lags, K]^T
-//       where X are the CP-stripped samples (both real GEMMs of estimator.py:77-80 in
-//       one contraction: Re and Im are separate rows) and C[lag, k] = chip[(k - lag) mod M]
-//       are the stacked lag-window rows of batched_lag_rows (estimator.py:62-65,114-117).
-//       C is never materialised: every lag-window row block and every K step is a view
-//       into one resident "Hankel table" of 16-byte chip windows in shared memory (see
-//       DESIGN.md "circulant operand"), so the circulant costs no HBM/L2 traffic and no
-//       pipeline stage space.
+//   K1  k_lfsr / k_build_circulant : generate_mseq (pn.py:109-138) on the device and the
+//       stacked lag-window rows C[j*L+l, k] = chip[(k - s_j - l) mod M]
+//       (batched_lag_rows, estimator.py:62-65,114-117) as a 16-bit K-major operand.
+//   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the received
+//       f32 (I,Q) samples into 16-bit rows (frame, batch, rx, re|im) x K.  Only used by
+//       the two-pass path; the fused K3 does this itself.
+//   K3  k_correlate : tcgen05 UMMA   D[rows, lags] = X[rows, K] . C[lags, K]^T
+//       (both real GEMMs of estimator.py:77-80 in one contraction: Re and Im are separate
+//       rows of X).  Two CTAs of a cluster share one 128-row sample tile X (converted once,
+//       copied to the peer over DSMEM / TMA-multicast) and each accumulates half of the lag
+//       columns in its own double-buffered TMEM, so the epilogue of one tile overlaps the
+//       MMAs of the next.
 //   K4  fused into K3's epilogue: x 1/M, Re/Im pairing, per-transmitter window demux into
 //       taps[f, r, t, l] (experiments.py:206-207) and optional sum|e|, sum|e|^2 and
 //       non-finite count vs. truth (metrics.py:19-25 + the north-star MSE).
@@ -41,11 +40,11 @@ using namespace pnce;
 
 namespace {
 
-constexpr int kBM = 128;       // sample rows per CTA (UMMA M = 256 per pair)
+constexpr int kBM = 128;       // sample rows per UMMA (M)
 constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
 constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
 constexpr int kSmemLimit = 227 * 1024;
-constexpr uint32_t kStageA = kBM * kBK * 2;  // 16 KB A stage per CTA
+constexpr uint32_t kStageA = kBM * kBK * 2;  // 16 KB sample tile per stage
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -67,7 +66,13 @@ int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
-// ------------------------------------------------------------------ K1: LFSR
+template <typename T>
+__device__ __forceinline__ T to16(float v) {
+    if constexpr (std::is_same<T, __half>::value) return __float2half_rn(v);
+    else return __float2bfloat16_rn(v);
+}
+
+// ------------------------------------------------------------------ K1: LFSR + circulant rows
 // One thread runs the Fibonacci LFSR for one period (pn.py:115-137):
 // out = MSB, fb = parity(state & tap_mask), state = ((state << 1) | fb) & mask.
 __global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m, int* period_out) {
@@ -87,10 +92,25 @@ __global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* ch
     *period_out = n;
 }
 
+// Stacked lag-window rows, K-major, zero padded: C[n, k] for n < rows_alloc, k < k_pad,
+// lag(n) = floor(M/N_b) * (n / L) + n % L  (shift_for_transmitter + window lag).
 template <typename T>
-__device__ __forceinline__ T to16(float v) {
-    if constexpr (std::is_same<T, __half>::value) return __float2half_rn(v);
-    else return __float2bfloat16_rn(v);
+__global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m, int k_pad, int r_total,
+                                  int rows_alloc, int l, int spacing) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)rows_alloc * k_pad;
+    for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(idx / k_pad);
+        const int k = (int)(idx % k_pad);
+        float v = 0.0f;
+        if (n < r_total && k < m) {
+            const int lag = (spacing * (n / l) + (n % l)) % m;
+            int ci = k - lag;
+            if (ci < 0) ci += m;
+            v = chips[ci];
+        }
+        a[idx] = to16<T>(v);
+    }
 }
 
 // ------------------------------------------------------------------ K2: pack
@@ -123,30 +143,33 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
 
 // ------------------------------------------------------------------ K3+K4
 // Variants (template MODE):
-//   kModePacked   : sample rows = the packed 16-bit operand of K2, TMA-loaded;
+//   kModePacked   : sample rows = the packed 16-bit operand of K2 (TMA, multicast to the pair);
 //   kModeFusedTma : sample rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
 //                   converted (remove_cp + de-interleave + fp16/bf16) by converter warps
 //                   straight into the 128B-swizzled UMMA A stage -- K2 fused away;
 //   kModeFusedLdg : as above, converters LDG the f32 rows (fallback for row strides that
 //                   are not 16-byte multiples).
-// Warp roles (16 warps, both CTAs unless noted):
-//   0 TMA producer (packed rows)       1 MMA issuer (leader CTA)      2 raw-row TMA producer
-//   3 spare                            4-7 converters (fused)         8-15 epilogue
+// Pair split (CorrParams::split):
+//   1 (lags > 256): both CTAs of the cluster work on the SAME 128-row tile; each converts
+//     half of its 64 links and bulk-copies them to the peer, each accumulates half of the
+//     tile's lag columns;
+//   0 (lags <= 256): each CTA owns its own 128 rows and all lag columns (no sharing).
+// Warp roles (16 warps):
+//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer      2 raw-row TMA producer
+//   3 spare                                          4-11 converters   12-15 epilogue
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
 constexpr int kWarps = 16;
 constexpr int kThreadsK3 = kWarps * 32;
 constexpr int kConvWarp0 = 4;
-constexpr int kConvWarps = 4;
-constexpr int kEpiWarp0 = 8;
-constexpr int kEpiWarps = 8;
-constexpr int kLinksPerTile = kBM / 2;                                          // 64 (re, im) row pairs
-constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
+constexpr int kConvWarps = 8;
+constexpr int kEpiWarp0 = 12;
+constexpr int kEpiWarps = 4;
 constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
-constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;  // 64 links: 33 KB
-constexpr int kMaxUnitsPerGroup = 16;
+constexpr uint32_t kRawRowBytes = kRawRowFloats * 4;
+constexpr int kConvBarId = 1;               // named barrier of the converter warps
 
 #ifdef PNCE_DIAG_TRACE
-// Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
+// Diagnostic timeline (globaltimer ns) for the first two CTAs: [cta][slot][index].
 constexpr int kTraceSlots = 16, kTraceMax = 512;
 __device__ long long g_trace[2 * kTraceSlots * kTraceMax];
 __device__ __forceinline__ long long gtimer() {
@@ -166,29 +189,25 @@ __device__ __forceinline__ long long gtimer() {
 #endif
 
 struct CorrParams {
-    int64_t total_rows;   // n_frames * n_batches * n_r * 2
-    int32_t m_tiles;      // 256-row tiles (one per CTA pair)
-    int32_t n_groups;     // lag-unit groups per tile
-    int32_t units_per_group;
-    int32_t n_units;
-    int32_t nh;           // lag rows per CTA half of one unit (unit MMA N = 2*nh)
-    int32_t g_cols;       // accumulator columns per group = units_per_group * 2 * nh
-    int32_t acc_stages;   // TMEM accumulator buffers
+    int64_t total_rows;  // n_frames * n_batches * n_r * 2
+    int32_t split;       // 1: pair shares a 128-row tile and splits its lag columns
+    int32_t m_tiles;     // pair tiles along the rows
+    int32_t n_groups;    // lag-column groups per tile
+    int32_t gc;          // accumulator columns per CTA per group (= n_mma * nm)
+    int32_t n_mma;       // MMAs per k-step, N = nm each
+    int32_t nm;
+    int32_t acc_stages;  // TMEM accumulator buffers
     int32_t k_blocks;
-    int32_t stages;       // A stages
-    int32_t raw_stages;   // FusedTma: f32 staging ring depth
-    int32_t table_rows;   // Hankel table rows (16 B each)
-    int32_t sigma;        // lag shift of the peer CTA's half == table shift of rank 1
-    uint32_t table_bytes; // 1024-aligned
+    int32_t stages;      // A+B stages
+    int32_t raw_stages;  // FusedTma: f32 staging ring depth
+    int32_t conv_links;  // links converted per CTA per tile (32 split / 64 otherwise)
+    uint32_t stage_bytes;
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
     int32_t m, c, samples;  // PN length, CP length, samples per received row
     int32_t bf16;
     float inv_m;
-    const float* chips;     // device chips (K1 output)
-    const int32_t* unit_mu; // per unit: lag of B row 0 in the leader's half
-    const int2* chunk_map;  // per unit, per 8-column chunk: {R index of its first column, first valid col}
     const float* iq;
     float* taps;
     const float* truth;
@@ -200,10 +219,7 @@ struct ConvTask {
     float re[8], im[8];
 };
 
-__device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, int kb, int task, ConvTask& t) {
-    const int link_local = task >> 3;
-    const int chunk = task & 7;
-    const int64_t q = link0 + link_local;
+__device__ __forceinline__ void conv_load(const CorrParams& p, int64_t q, int kb, int chunk, ConvTask& t) {
     const int k0 = kb * kBK + chunk * 8;
     const bool ok = q < (p.total_rows >> 1);
     const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
@@ -229,10 +245,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row)
     return base + row * 128 + ((((byte_in_row >> 4) ^ (row & 7))) << 4) + (byte_in_row & 15);
 }
 
-__device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask& t, int bf16) {
-    const int link_local = task >> 3;
-    const int chunk = task & 7;
-    const int row_re = 2 * link_local, row_im = row_re + 1;
+__device__ __forceinline__ void conv_store(uint32_t sa, int row_re, int chunk, const ConvTask& t, int bf16) {
     uint4 vr, vi;
     vr.x = pack2(t.re[0], t.re[1], bf16);
     vr.y = pack2(t.re[2], t.re[3], bf16);
@@ -243,15 +256,14 @@ __device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask
     vi.z = pack2(t.im[4], t.im[5], bf16);
     vi.w = pack2(t.im[6], t.im[7], bf16);
     st_shared_v4(swz(sa, row_re, chunk * 16), vr);
-    st_shared_v4(swz(sa, row_im, chunk * 16), vi);
+    st_shared_v4(swz(sa, row_re + 1, chunk * 16), vi);
 }
 
 // Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
-// The even lane owns accumulator columns 0..7 of the slice, the odd lane 8..15; the
-// 8 columns of an 8-chunk hold DEScending lags (Hankel order): column i <-> R index
-// rc0 - i, valid for i >= first_valid.
-__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok, int2 cm,
-                                          int n_valid, int64_t out_base, float& s_abs, float& s_sq, float& s_bad) {
+// Re/Im pairing: the even lane (Re row) keeps columns 0..7, the odd lane (Im row) 8..15.
+__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok,
+                                          int n_first, int n_valid, int64_t out_base, float& s_abs, float& s_sq,
+                                          float& s_bad) {
     float x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -259,37 +271,33 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
     }
     if (!row_ok) return;
-    // o[2q], o[2q+1] = complex value for R index rc0 - 7 + q (ascending addresses)
     float o[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int i = 7 - q;
-        o[2 * q] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
-        o[2 * q + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
+    for (int i = 0; i < 8; ++i) {
+        o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
+        o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
     }
-    const int r_lo = cm.x - 7;                 // R index of o[0]
-    const int64_t g = out_base + r_lo;         // complex index of o[0]
-    const bool all = cm.y == 0 && cm.x < n_valid && r_lo >= 0;
+    const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
 #ifdef PNCE_DIAG_NO_STORE
-    if (o[0] == 12345.678f) p.taps[out_base] = o[1];  // keep the work, drop the stores
+    if (o[0] == 12345.678f) p.taps[g] = o[1];  // keep the work, drop the stores
     return;
 #endif
-    if (all && (g & 3) == 0) {
+    if (n_first + 8 <= n_valid && (g & 3) == 0) {
         float* dst = p.taps + 2 * g;
         st_global_v8(dst, *reinterpret_cast<const float(*)[8]>(&o[0]));
         st_global_v8(dst + 8, *reinterpret_cast<const float(*)[8]>(&o[8]));
         if (p.stats != nullptr) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (!(isfinite(o[2 * q]) && isfinite(o[2 * q + 1]))) s_bad += 1.f;
+            for (int i = 0; i < 8; ++i)
+                if (!(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
         }
         if (p.truth != nullptr) {
             float h[16];
             ld_global_nc_v8(p.truth + 2 * g, *reinterpret_cast<float(*)[8]>(&h[0]));
             ld_global_nc_v8(p.truth + 2 * g + 8, *reinterpret_cast<float(*)[8]>(&h[8]));
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float dx = o[2 * q] - h[2 * q], dy = o[2 * q + 1] - h[2 * q + 1];
+            for (int i = 0; i < 8; ++i) {
+                const float dx = o[2 * i] - h[2 * i], dy = o[2 * i + 1] - h[2 * i + 1];
                 const float sq = dx * dx + dy * dy;
                 s_sq += sq;
                 s_abs += sqrtf(sq);
@@ -299,14 +307,13 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         float2* taps = reinterpret_cast<float2*>(p.taps);
         const float2* truth = reinterpret_cast<const float2*>(p.truth);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int r = r_lo + q;
-            if (7 - q >= cm.y && r >= 0 && r < n_valid) {
-                taps[g + q] = make_float2(o[2 * q], o[2 * q + 1]);
-                if (p.stats != nullptr && !(isfinite(o[2 * q]) && isfinite(o[2 * q + 1]))) s_bad += 1.f;
+        for (int i = 0; i < 8; ++i) {
+            if (n_first + i < n_valid) {
+                taps[g + i] = make_float2(o[2 * i], o[2 * i + 1]);
+                if (p.stats != nullptr && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
                 if (truth != nullptr) {
-                    const float2 h = __ldg(truth + g + q);
-                    const float dx = o[2 * q] - h.x, dy = o[2 * q + 1] - h.y;
+                    const float2 h = __ldg(truth + g + i);
+                    const float dx = o[2 * i] - h.x, dy = o[2 * i + 1] - h.y;
                     const float sq = dx * dx + dy * dy;
                     s_sq += sq;
                     s_abs += sqrtf(sq);
@@ -316,70 +323,60 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
     }
 }
 
-// CTA pair (cluster 2x1): the pair owns 256 sample rows (128 per CTA, UMMA M = 256,
-// cta_group::2); the leader CTA (rank 0) issues every MMA.  A lag "unit" is one MMA of
-// N = 2*nh lags: the leader's B half covers nh consecutive (descending) lags, the peer's
-// half the nh lags shifted by sigma -- both halves are views of the CTA's own Hankel
-// table (the peer's table is pre-shifted by sigma), so one descriptor serves both.
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
-k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
+k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
+            const CorrParams p) {
     constexpr bool FUSED = MODE != kModePacked;
     constexpr bool RAW = MODE == kModeFusedTma;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // [Hankel table][A stages][1 KB barrier block][raw f32 stages]
+    // [A+B stages][1 KB barrier block][raw f32 stages]
     const int S = p.stages;
-    uint8_t* table = smem;
-    uint8_t* a_base = smem + p.table_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(a_base + (size_t)S * kStageA);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint64_t* raw_full = tempty + 2;
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
-    uint8_t* raw_base = a_base + (size_t)S * kStageA + 1024;
+    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
+    const uint32_t raw_stage_bytes = (uint32_t)p.conv_links * kRawRowBytes;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    const bool leader = rank == 0;
+    const uint32_t peer = rank ^ 1u;
+    const bool split = p.split != 0;
+    const uint16_t pair_mask = 3;
+    // bytes of the half sample tile each CTA converts and ships to its peer (split mode)
+    const uint32_t half_a = kStageA / 2;
 
-    // ---- Hankel table: row rho (16 B) = chips[(rho + jj - rank*sigma) mod M], jj = 0..7
-    {
-        const int shift = (int)((p.m - (int)(((int64_t)rank * p.sigma) % p.m)) % p.m);
-        const int total = p.table_rows * 8;
-        for (int idx = threadIdx.x; idx < total; idx += kThreadsK3) {
-            int ci = (idx >> 3) + (idx & 7) + shift;
-            ci %= p.m;
-            const float v = __ldg(p.chips + ci);
-            if (p.bf16) reinterpret_cast<__nv_bfloat16*>(table)[idx] = __float2bfloat16_rn(v);
-            else reinterpret_cast<__half*>(table)[idx] = __float2half_rn(v);
-        }
-        fence_proxy_async_smem();
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            // Leader: (packed) the producer's expect_tx arrive; (fused) the converter warps
-            // of BOTH CTAs -- the peer's TMA bytes and converter arrives land here too.
-            mbar_init(&full[s], FUSED ? 2 * kConvWarps : 1);
-            mbar_init(&empty[s], 1);
+            // full: the producer's expect_tx arrive (+ the converter group's arrive when fused);
+            //       the peer's TMA-multicast / bulk-copied half tile lands as transaction bytes.
+            // empty: released by the MMA of every CTA that reads this stage's sample tile.
+            mbar_init(&full[s], FUSED ? 2 : 1);
+            mbar_init(&empty[s], split ? 2 : 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * kEpiWarps);
+            mbar_init(&tempty[a], kEpiWarps);
         }
         if (RAW) {
             for (int s = 0; s < p.raw_stages; ++s) {
                 mbar_init(&raw_full[s], 1);
-                mbar_init(&raw_empty[s], kConvWarps);
+                mbar_init(&raw_empty[s], 1);
             }
         }
         fence_mbar_init();
     }
-    if (warp == 0 && lane == 0 && MODE != kModeFusedLdg) tma_prefetch(&tm_in);
-    if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
+    if (warp == 0 && lane == 0) {
+        if (MODE != kModeFusedLdg) tma_prefetch(&tm_in);
+        tma_prefetch(&tm_circ);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
@@ -390,74 +387,86 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
     const int total_tiles = p.m_tiles * p.n_groups;
     const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
+    // first sample row of this CTA's MMA tile, and first link this CTA converts
+    auto tile_row0 = [&](int mt) -> int64_t {
+        return split ? (int64_t)mt * kBM : (int64_t)mt * 2 * kBM + (int64_t)rank * kBM;
+    };
+    auto conv_link0 = [&](int mt) -> int64_t { return tile_row0(mt) / 2 + (split ? (int64_t)rank * 32 : 0); };
+    // accumulator columns of this CTA in group g
+    auto col0 = [&](int g) -> int { return split ? (2 * g + (int)rank) * p.gc : g * p.gc; };
 
     if (warp == 0) {
-        if (!FUSED && lane == 0) {
-            // ===== TMA producer: packed sample rows; bytes land on the leader's barrier
+        if (lane == 0) {
+            // ===== TMA producer: circulant rows (+ packed sample rows)
             const uint64_t pol_in = policy_evict_first();
+            const uint64_t pol_circ = policy_evict_last();
+            const uint32_t b_bytes = (uint32_t)p.gc * kBK * 2;
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
-                const int mt = (cid + ti * n_clusters) / p.n_groups;
+                const int tile = cid + ti * n_clusters;
+                const int mt = tile / p.n_groups;
+                const int g = tile - mt * p.n_groups;
                 const int stage = j % S;
                 mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
                 TRACE(0, j);
-                if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageA);
-                tma_load_2d_pair(a_base + (size_t)stage * kStageA, &tm_in, mapa_shared(smem_u32(&full[stage]), 0),
-                                 kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
+                uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+                uint8_t* sb = sa + kStageA;
+                // this CTA receives: its B rows, plus (fused split) the peer's half tile, or
+                // (packed) the whole tile (own TMA + peer multicast in split mode)
+                const uint32_t tx = b_bytes + (FUSED ? (split ? half_a : 0u) : kStageA);
+                mbar_arrive_expect_tx(&full[stage], tx);
+                if (!FUSED) {
+                    if (split)
+                        tma_load_2d_mc(sa + rank * half_a, &tm_in, &full[stage], kb * kBK,
+                                       (int)(tile_row0(mt) + rank * 64), pair_mask, pol_in);
+                    else
+                        tma_load_2d(sa, &tm_in, &full[stage], kb * kBK, (int)tile_row0(mt), pol_in);
+                }
+                for (int jj = 0; jj < p.n_mma; ++jj)
+                    tma_load_2d(sb + (size_t)jj * p.nm * kBK * 2, &tm_circ, &full[stage], kb * kBK,
+                                col0(g) + jj * p.nm, pol_circ);
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
-            // ===== MMA issuer (leader CTA, single thread) for the whole pair
-            const uint32_t tbl = smem_u32(table);
+        if (lane == 0) {
+            // ===== MMA issuer (single thread): cta_group::1, M = 128, N = nm
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int ti = 0; ti < my_tiles; ++ti) {
-                const int g = (cid + ti * n_clusters) % p.n_groups;
-                const int u0 = g * p.units_per_group;
-                const int nu = min(p.units_per_group, p.n_units - u0);
-                int rho[kMaxUnitsPerGroup];  // Hankel start row per unit, advanced by 16 per k-step
-#pragma unroll
-                for (int u = 0; u < kMaxUnitsPerGroup; ++u)
-                    if (u < nu) rho[u] = (p.m - __ldg(p.unit_mu + u0 + u) % p.m) % p.m;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 TRACE(1, ti);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.gc);
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const int j = ti * p.k_blocks + kb;
                     const int stage = j % S;
-#ifndef PNCE_DIAG_NO_FULLWAIT
                     mbar_wait(&full[stage], (uint32_t)(j / S) & 1u);
-#endif
                     TRACE(2, j);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(a_base + (size_t)stage * kStageA);
+                    const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                    const uint32_t sb = sa + kStageA;
 #pragma unroll
                     for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
-#pragma unroll
-                        for (int u = 0; u < kMaxUnitsPerGroup; ++u) {
-                            if (u < nu) {
-                                const uint64_t bd = make_sdesc(tbl + (uint32_t)rho[u] * 16u, 128, 128, 0);
-                                umma_f16_ss_pair(d_tmem + (uint32_t)(u * 2 * p.nh), ad, bd, p.idesc, (kb | ks) != 0);
-                                rho[u] += kUmmaK;
-                                if (rho[u] >= p.m) rho[u] -= p.m;
-                            }
+                        for (int jj = 0; jj < p.n_mma; ++jj) {
+                            const uint64_t bd = make_sdesc(sb + (uint32_t)(jj * p.nm * kBK * 2) + ks * 32, 16, 1024, 2);
+                            umma_f16_ss(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
                         }
                     }
-                    umma_commit_pair(&empty[stage]);
+                    // the stage's sample tile is read by both CTAs in split mode: free it in both
+                    if (split) umma_commit_mc(&empty[stage], pair_mask);
+                    else umma_commit(&empty[stage]);
                     TRACE(3, j);
                 }
-                umma_commit_pair(&tfull[acc]);
+                umma_commit(&tfull[acc]);
                 if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else if (warp == 2) {
         if (RAW && lane == 0) {
-            // ===== raw-row producer: TMA the f32 (I,Q) rows of this CTA's 64 links for one
-            // K-block (64 links x 64 samples x 8 B + slack) into the staging ring.
+            // ===== raw-row producer: TMA the f32 (I,Q) rows of the links this CTA converts
+            // for one K-block (64 samples x 8 B + slack per link) into the staging ring.
             const uint64_t pol = policy_evict_first();
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
@@ -470,40 +479,43 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
                 mbar_arrive(&raw_full[rs]);
                 (void)pol; (void)mt; (void)kb;
 #else
-                mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
+                mbar_arrive_expect_tx(&raw_full[rs], raw_stage_bytes);
                 // box start rounded down to a 16-byte boundary; converters skip the slack
-                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs], (2 * (p.c + kb * kBK)) & ~3,
-                            (mt * 2 + (int)rank) * kLinksPerTile, pol);
+                tma_load_2d(raw_base + (size_t)rs * raw_stage_bytes, &tm_in, &raw_full[rs],
+                            (2 * (p.c + kb * kBK)) & ~3, (int)conv_link0(mt), pol);
 #endif
             }
         }
     } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
         if (FUSED) {
+            // ===== converters: this CTA's links -> rows (2*link, 2*link+1) of the A stage;
+            // in split mode these are rows [64*rank, 64*rank+64) and are bulk-copied to the peer.
             const int cw = warp - kConvWarp0;
-            const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
+            const bool elected = cw == 0 && lane == 0;
+            const int row_base = split ? 64 * (int)rank : 0;
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
                 const int stage = j % S;
-                const uint32_t sa = smem_u32(a_base + (size_t)stage * kStageA);
+                uint8_t* sa_ptr = smem + (size_t)stage * p.stage_bytes;
+                const uint32_t sa = smem_u32(sa_ptr);
+                int rs = 0;
                 if (RAW) {
-                    // staged f32 rows -> A stage.  Warp w converts links w, w+4, ...; lane l
-                    // handles samples 2l, 2l+1 (one conflict-free LDS of the staged row, two
-                    // STS.32 into the Re / Im rows).
-                    const int rs = j % p.raw_stages;
+                    // staged rows -> A stage.  Warp w converts links w, w+8, ...; lane l handles
+                    // samples 2l, 2l+1 (one conflict-free LDS of the staged row, two STS.32).
+                    rs = j % p.raw_stages;
                     mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
-                    if (cw == 0 && lane == 0) TRACE(7, j);
+                    if (elected) TRACE(7, j);
                     mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
-                    if (cw == 0 && lane == 0) TRACE(8, j);
+                    if (elected) TRACE(8, j);
                     const int slack = (2 * (p.c + kb * kBK)) & 3;  // 0 or 2 floats
-                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * kRawStageBytes) + slack * 4 + lane * 16;
+                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * raw_stage_bytes) + slack * 4 + lane * 16;
                     const int k = kb * kBK + 2 * lane;
                     const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
 #ifndef PNCE_DIAG_NO_CONV
 #pragma unroll 4
-                    for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
-                        const int link_local = cw + kConvWarps * i;
-                        const uint32_t src = raw + link_local * (kRawRowFloats * 4);
+                    for (int i = cw; i < p.conv_links; i += kConvWarps) {
+                        const uint32_t src = raw + i * kRawRowBytes;
                         float4 v;
                         if (slack == 0) {
                             v = ld_shared_v4f(src);
@@ -514,47 +526,50 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
                         }
                         if (!ok0) { v.x = 0.f; v.y = 0.f; }
                         if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                        st_shared_u32(swz(sa, 2 * link_local, lane * 4), pack2(v.x, v.z, p.bf16));
-                        st_shared_u32(swz(sa, 2 * link_local + 1, lane * 4), pack2(v.y, v.w, p.bf16));
+                        const int row = row_base + 2 * i;
+                        st_shared_u32(swz(sa, row, lane * 4), pack2(v.x, v.z, p.bf16));
+                        st_shared_u32(swz(sa, row + 1, lane * 4), pack2(v.y, v.w, p.bf16));
                     }
 #else
                     (void)raw; (void)ok0; (void)ok1;
 #endif
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        // the proxy fence completed this warp's STS; plain (CTA-scope release)
-                        // arrive on the leader's barrier, no GPU-scope membar
-                        mbar_arrive_remote(full_leader0 + (uint32_t)(stage * 8));
-                        mbar_arrive(&raw_empty[rs]);
-                        if (cw == 0) TRACE(9, j);
-                    }
                 } else {
-                    // LDG fallback: 4 tasks (link, 8-sample chunk) per thread
+                    // LDG fallback: (link, 8-sample chunk) tasks
                     const int mt = (cid + ti * n_clusters) / p.n_groups;
-                    const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
+                    const int64_t link0 = conv_link0(mt);
                     const int ct = cw * 32 + lane;
-                    ConvTask buf[kTasksPerThread];
+                    const int tasks = p.conv_links * 8;
+                    ConvTask buf[2];
+                    const int n_my = (tasks - ct + kConvWarps * 32 - 1) / (kConvWarps * 32);
 #pragma unroll
-                    for (int i = 0; i < kTasksPerThread; ++i) conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
+                    for (int i = 0; i < 2; ++i)
+                        if (i < n_my) conv_load(p, link0 + ((ct + i * kConvWarps * 32) >> 3), kb,
+                                                (ct + i * kConvWarps * 32) & 7, buf[i]);
                     mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
 #pragma unroll
-                    for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(full_leader0 + (uint32_t)(stage * 8));
+                    for (int i = 0; i < 2; ++i) {
+                        const int t = ct + i * kConvWarps * 32;
+                        if (i < n_my) conv_store(sa, row_base + 2 * (t >> 3), t & 7, buf[i], p.bf16);
+                    }
+                }
+                // all converter warps' STS -> async proxy; then one thread publishes
+                fence_proxy_async_smem();
+                named_bar_sync(kConvBarId, kConvWarps * 32);
+                if (elected) {
+                    if (split) {
+                        // ship our half tile to the peer; its bytes complete the peer's full barrier
+                        bulk_copy_s2s(mapa_shared(sa + (uint32_t)row_base * 128, peer), sa_ptr + row_base * 128, half_a,
+                                      mapa_shared(smem_u32(&full[stage]), peer));
+                    }
+                    mbar_arrive(&full[stage]);
+                    if (RAW) mbar_arrive(&raw_empty[rs]);
+                    TRACE(9, j);
                 }
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ===== epilogue (both CTAs): TMEM lane quarter = warp % 4, column half = (warp-8)/4
+        // ===== epilogue: TMEM lane quarter = warp % 4; all of this CTA's columns
         const int quarter = warp & 3;
-        const int half = (warp - kEpiWarp0) >> 2;
-        const int cph = ((p.g_cols + 1) / 2 + 15) / 16 * 16;
-        const int c_begin = min(p.g_cols, half * cph);
-        const int c_end = min(p.g_cols, c_begin + cph);
-        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
-        const int chunks_per_unit = (2 * p.nh) / 8;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int ti = 0; ti < my_tiles; ++ti) {
@@ -565,7 +580,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
             if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
             tc_fence_after();
 
-            const int64_t row = (int64_t)mt * 2 * kBM + (int64_t)rank * kBM + quarter * 32 + lane;
+            const int64_t row = tile_row0(mt) + quarter * 32 + lane;
             const bool row_ok = row < p.total_rows;
             const bool odd = (lane & 1) != 0;
             const int64_t link = row >> 1;
@@ -576,34 +591,30 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
             const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
             const int n_valid = n_tx * p.l;
             const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
-            const int2* cmap = p.chunk_map + (size_t)g * p.units_per_group * chunks_per_unit;
-            const int n_map = min(p.units_per_group, p.n_units - g * p.units_per_group) * chunks_per_unit;
             float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
-            auto chunk_of = [&](int col) -> int2 {
-                const int ci = (col >> 3) + (odd ? 1 : 0);
-                return ci < n_map ? __ldg(cmap + ci) : make_int2(0, 8);
-            };
 
-            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.g_cols);
+            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.gc);
+            const int n0 = col0(g) + (odd ? 8 : 0);
             // 32-column chunks (two 16-column slices each); the next chunk's TMEM load is
             // in flight while the current one is paired, scaled and stored.
             uint32_t va[32], vb[32];
-            int c0 = c_begin;
+            int c0 = 0;
+            const int c_end = p.gc;
             if (c0 + 32 <= c_end) {
                 tmem_ld32_nowait(t_row + c0, va);
                 tmem_wait_ld();
                 while (true) {
                     const bool more = c0 + 64 <= c_end;
                     if (more) tmem_ld32_nowait(t_row + c0 + 32, vb);
-                    epi_slice(p, va, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, va + 16, odd, row_ok, chunk_of(c0 + 16), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va + 16, odd, row_ok, n0 + c0 + 16, n_valid, out_base, s_abs, s_sq, s_bad);
                     c0 += 32;
                     if (!more) break;
                     tmem_wait_ld();
                     const bool more2 = c0 + 64 <= c_end;
                     if (more2) tmem_ld32_nowait(t_row + c0 + 32, va);
-                    epi_slice(p, vb, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, vb + 16, odd, row_ok, chunk_of(c0 + 16), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb + 16, odd, row_ok, n0 + c0 + 16, n_valid, out_base, s_abs, s_sq, s_bad);
                     c0 += 32;
                     if (!more2) break;
                     tmem_wait_ld();
@@ -612,12 +623,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
             if (c0 < c_end) {  // 16-column remainder
                 tmem_ld16_nowait(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(va));
                 tmem_wait_ld();
-                epi_slice(p, va, odd, row_ok, chunk_of(c0), n_valid, out_base, s_abs, s_sq, s_bad);
+                epi_slice(p, va, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
             }
-            // this warp's share of the accumulator is drained -> tell the leader's MMA warp
+            // accumulator buffer drained -> hand it back to this CTA's MMA thread
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
+            if (lane == 0) mbar_arrive(&tempty[acc]);
             if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
 
@@ -654,10 +665,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const CorrParams p) {
 
     __syncwarp();
     tc_fence_before();
-    cluster_sync_all();
+    cluster_sync_all();  // the peer may still be writing our smem / arriving on our barriers
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc_pair(tmem_base, p.tmem_cols);
+        tmem_dealloc(tmem_base, p.tmem_cols);
     }
 }
 
@@ -675,13 +686,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// Packed sample rows: 2-D [rows][k_pad] 16-bit, box [128 rows][64], 128B swizzle.
-pnce_status_t make_tmap_packed(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, int bf16) {
+// 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128B swizzle.
+pnce_status_t make_tmap16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                          int bf16) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -690,15 +702,16 @@ pnce_status_t make_tmap_packed(CUtensorMap* map, const void* base, uint64_t cols
     return PNCE_OK;
 }
 
-// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][132 floats]
-// (one K-block of 64 (I,Q) samples for 64 links + 16 B slack so the box start can be
-// rounded down to a 16-byte boundary), no swizzle.
-pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows) {
+// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [links_box][132 floats]
+// (one K-block of 64 (I,Q) samples + 16 B slack so the box start can be rounded down to
+// a 16-byte boundary), no swizzle.
+pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows,
+                            uint32_t links_box) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {row_floats, rows};
     cuuint64_t strides[1] = {row_floats * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, (cuuint32_t)kLinksPerTile};
+    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, links_box};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -707,85 +720,43 @@ pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_fl
     return PNCE_OK;
 }
 
-// Lag layout: which lag rows each MMA "unit" covers and where each accumulator column
-// lands in the taps.
-struct LagLayout {
-    int nh = 8;                 // rows per CTA half (multiple of 8, <= 128)
-    int sigma = 0;              // lag shift of the peer half (Hankel table shift of rank 1)
-    std::vector<int32_t> mu;    // per unit: lag of B row 0 of the leader's half
-    std::vector<int2> chunks;   // per unit, per 8-column chunk: {R index of column 0, first valid column}
-};
-
-LagLayout plan_lags(const pnce_cfg_t& c) {
-    LagLayout L;
-    const int M = c.m, Lw = c.l, Nb = c.n_batch;
-    const int delta = M / Nb;
-    auto r8 = [](int x) { return (x + 7) / 8 * 8; };
-    const bool pair_mode = Lw <= 128 && Nb >= 2 && delta > Lw;
-    if (pair_mode) {
-        // unit u = windows (2u, 2u+1): the peer half is the next window, sigma = delta
-        L.nh = r8(Lw);
-        L.sigma = delta;
-        const int units = (Nb + 1) / 2;
-        for (int u = 0; u < units; ++u) {
-            L.mu.push_back(2 * u * delta + L.nh - 1);
-            for (int h = 0; h < 2; ++h) {
-                const int j = 2 * u + h;
-                for (int q = 0; q < L.nh / 8; ++q) {
-                    const int l0 = L.nh - 1 - 8 * q;  // tap of column 0 of this chunk (descending)
-                    int first_valid = std::max(0, std::min(8, l0 - Lw + 1));
-                    if (j >= Nb) first_valid = 8;
-                    L.chunks.push_back(make_int2(j * Lw + l0, first_valid));
-                }
-            }
-        }
-        return L;
-    }
-    // chunk mode: windows split into units of 2*nh contiguous lags (peer = next nh lags)
-    struct Window { int start, len, r_off; };
-    std::vector<Window> wins;
-    if (delta == Lw || Nb == 1) wins.push_back({0, Nb * Lw, 0});  // one contiguous lag range
-    else
-        for (int j = 0; j < Nb; ++j) wins.push_back({j * delta, Lw, j * Lw});
-    const int maxlen = wins[0].len;
-    L.nh = std::min(128, r8((maxlen + 1) / 2));
-    L.sigma = L.nh;
-    for (const Window& w : wins) {
-        const int units = (w.len + 2 * L.nh - 1) / (2 * L.nh);
-        for (int u = 0; u < units; ++u) {
-            const int base = 2 * L.nh * u;
-            L.mu.push_back(w.start + base + L.nh - 1);
-            for (int h = 0; h < 2; ++h)
-                for (int q = 0; q < L.nh / 8; ++q) {
-                    const int l0 = base + h * L.nh + L.nh - 1 - 8 * q;
-                    const int first_valid = std::max(0, std::min(8, l0 - w.len + 1));
-                    L.chunks.push_back(make_int2(w.r_off + l0, first_valid));
-                }
-        }
-    }
-    return L;
-}
-
-// Unit grouping for one K3 variant.
+// Lag-column tiling (shared by all K3 variants).
 struct Tiling {
-    int units_per_group;
-    int n_groups;
-    int g_cols;
+    int split;       // pair shares the sample tile, splits the lag columns
+    int n_groups;    // column groups per tile
+    int gc;          // accumulator columns per CTA per group
+    int n_mma, nm;   // MMAs per k-step and their N
     int acc_stages;
+    int rows_needed; // circulant rows the tiling addresses
     uint32_t tmem_cols;
+    uint32_t stage_bytes;
 };
 
-Tiling make_tiling(int n_units, int nh, int max_cols) {
+Tiling make_tiling(int r_total) {
     Tiling t{};
-    const int unit_cols = 2 * nh;
-    int per = std::max(1, std::min(std::min(n_units, kMaxUnitsPerGroup), max_cols / unit_cols));
-    t.n_groups = (n_units + per - 1) / per;
-    t.units_per_group = (n_units + t.n_groups - 1) / t.n_groups;
-    t.g_cols = t.units_per_group * unit_cols;
-    t.acc_stages = (2 * t.g_cols <= 512) ? 2 : 1;
+    const int r16 = (r_total + 15) / 16 * 16;
+    const int max_cta_cols = env_int("PNCE_TUNE_CTA_COLS", 256);
+    if (r16 <= max_cta_cols) {
+        t.split = 0;
+        t.n_groups = 1;
+        t.gc = r16;
+    } else {
+        t.split = 1;
+        t.n_groups = (r16 + 2 * max_cta_cols - 1) / (2 * max_cta_cols);
+        t.gc = ((r16 + 2 * t.n_groups - 1) / (2 * t.n_groups) + 15) / 16 * 16;
+    }
+    t.n_mma = (t.gc + 255) / 256;
+    t.nm = t.gc / t.n_mma;
+    if (t.nm * t.n_mma != t.gc || t.nm % 16 != 0) {  // keep N a multiple of 16
+        t.nm = (t.nm + 15) / 16 * 16;
+        t.gc = t.nm * t.n_mma;
+    }
+    t.acc_stages = (2 * t.gc <= 512) ? 2 : 1;
+    t.rows_needed = t.n_groups * t.gc * (t.split ? 2 : 1);
     uint32_t cols = 32;
-    while (cols < (uint32_t)(t.acc_stages * t.g_cols)) cols <<= 1;
+    while (cols < (uint32_t)(t.acc_stages * t.gc)) cols <<= 1;
     t.tmem_cols = cols;
+    t.stage_bytes = kStageA + (uint32_t)t.gc * kBK * 2;
     return t;
 }
 
@@ -794,21 +765,19 @@ Tiling make_tiling(int n_units, int nh, int max_cols) {
 struct pnce_plan {
     pnce_cfg_t cfg;
     int n_batches;
-    int k_pad;        // roundup(M, 64)
+    int r_total;     // N_b * L
+    int k_pad;       // roundup(M, 64)
     int num_sms;
-    LagLayout lags;
-    Tiling fused;     // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
-    Tiling packed;    // packed operand in: groups of <= 256 cols, double-buffered accumulator
-    int table_rows;
-    uint32_t table_bytes;
-    float* chips;         // device [m]
-    int32_t* unit_mu;     // device [n_units]
-    int2* chunk_map;      // device [n_units * 2nh/8]
+    Tiling tiling;
+    int rows_alloc;  // circulant rows allocated
+    float* chips;    // device [m]
+    void* circ;      // device [rows_alloc][k_pad] 16-bit
+    CUtensorMap tm_circ;
 };
 
 extern "C" {
 
-int32_t pnce_version(void) { return 200; }
+int32_t pnce_version(void) { return 300; }
 
 const char* pnce_last_error(void) { return g_err.c_str(); }
 
@@ -879,29 +848,41 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     pnce_plan* p = new pnce_plan();
     p->cfg = *cfg;
     p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
+    p->r_total = cfg->n_batch * cfg->l;
     p->k_pad = (cfg->m + kBK - 1) / kBK * kBK;
     p->num_sms = sms;
-    p->lags = plan_lags(*cfg);
-    const int n_units = (int)p->lags.mu.size();
-    p->fused = make_tiling(n_units, p->lags.nh, env_int("PNCE_TUNE_GROUP_FUSED", 512));
-    p->packed = make_tiling(n_units, p->lags.nh, env_int("PNCE_TUNE_GROUP_PACKED", 256));
-    p->table_rows = (cfg->m + p->lags.nh + 2 * kUmmaK + 7) / 8 * 8;
-    p->table_bytes = (uint32_t)((p->table_rows * 16 + 1023) / 1024 * 1024);
+    p->tiling = make_tiling(p->r_total);
+    p->rows_alloc = p->tiling.rows_needed;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    if (e == cudaSuccess) e = cudaMalloc(&p->unit_mu, sizeof(int32_t) * n_units);
-    if (e == cudaSuccess) e = cudaMalloc(&p->chunk_map, sizeof(int2) * p->lags.chunks.size());
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(p->unit_mu, p->lags.mu.data(), sizeof(int32_t) * n_units, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(p->chunk_map, p->lags.chunks.data(), sizeof(int2) * p->lags.chunks.size(),
-                            cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
     }
     s = pnce_generate_mseq(cfg->degree, cfg->tap_mask, cfg->state, p->chips, cfg->m, stream);
+    if (s != PNCE_OK) {
+        pnce_plan_destroy(p);
+        return s;
+    }
+    const int spacing = cfg->m / cfg->n_batch;
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    if (cfg->dtype == PNCE_DTYPE_BF16)
+        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad,
+                                                                  p->r_total, p->rows_alloc, cfg->l, spacing);
+    else
+        k_build_circulant<__half><<<blocks, 256, 0, st>>>(p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total,
+                                                           p->rows_alloc, cfg->l, spacing);
+    g_launches++;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        pnce_plan_destroy(p);
+        return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
+    }
+    s = make_tmap16(&p->tm_circ, p->circ, p->k_pad, p->rows_alloc, p->tiling.nm, cfg->dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
         return s;
@@ -928,8 +909,7 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
 pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
     if (!p) return PNCE_OK;
     if (p->chips) cudaFree(p->chips);
-    if (p->unit_mu) cudaFree(p->unit_mu);
-    if (p->chunk_map) cudaFree(p->chunk_map);
+    if (p->circ) cudaFree(p->circ);
     delete p;
     return PNCE_OK;
 }
@@ -958,8 +938,7 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     const int samples = c.c + c.m + c.l - 1;
     const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
     const int64_t work = links * (p->k_pad / 8);
-    const int64_t want = (work + 255) / 256;
-    const int blocks = (int)std::min<int64_t>(want, (int64_t)p->num_sms * 16);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)p->num_sms * 16);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (c.dtype == PNCE_DTYPE_BF16)
         k_pack_iq<__nv_bfloat16><<<blocks, 256, 0, st>>>(iq, (__nv_bfloat16*)packed, links, samples, c.c, c.m, p->k_pad);
@@ -975,28 +954,29 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
 namespace {
 
 // Shared launch setup for all K3 variants.
-pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, float* taps, const float* truth, double* stats,
-                          int64_t n_frames, CorrParams& prm) {
+pnce_status_t fill_params(const pnce_plan_t* p, float* taps, const float* truth, double* stats, int64_t n_frames,
+                          CorrParams& prm) {
     if ((reinterpret_cast<uintptr_t>(taps) & 7) || (truth && (reinterpret_cast<uintptr_t>(truth) & 7)))
         return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
     const pnce_cfg_t& c = p->cfg;
+    const Tiling& t = p->tiling;
     prm = CorrParams{};
     prm.total_rows = n_frames * p->n_batches * (int64_t)c.n_r * 2;
-    const int64_t m_tiles = (prm.total_rows + 2 * kBM - 1) / (2 * kBM);
+    const int64_t tile_rows = t.split ? kBM : 2 * kBM;
+    const int64_t m_tiles = (prm.total_rows + tile_rows - 1) / tile_rows;
     if (m_tiles * t.n_groups > INT32_MAX || prm.total_rows > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
+    prm.split = t.split;
     prm.m_tiles = (int32_t)m_tiles;
     prm.n_groups = t.n_groups;
-    prm.units_per_group = t.units_per_group;
-    prm.n_units = (int)p->lags.mu.size();
-    prm.nh = p->lags.nh;
-    prm.g_cols = t.g_cols;
+    prm.gc = t.gc;
+    prm.n_mma = t.n_mma;
+    prm.nm = t.nm;
     prm.acc_stages = t.acc_stages;
     prm.k_blocks = p->k_pad / kBK;
-    prm.table_rows = p->table_rows;
-    prm.table_bytes = p->table_bytes;
-    prm.sigma = p->lags.sigma;
-    prm.idesc = make_idesc_f16(2 * kBM, 2 * p->lags.nh, c.dtype == PNCE_DTYPE_BF16);
+    prm.conv_links = t.split ? 32 : 64;
+    prm.stage_bytes = t.stage_bytes;
+    prm.idesc = make_idesc_f16(kBM, t.nm, c.dtype == PNCE_DTYPE_BF16);
     prm.tmem_cols = t.tmem_cols;
     prm.n_r = c.n_r;
     prm.n_t = c.n_t;
@@ -1008,9 +988,6 @@ pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, float* taps, co
     prm.samples = c.c + c.m + c.l - 1;
     prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
     prm.inv_m = 1.0f / (float)c.m;
-    prm.chips = p->chips;
-    prm.unit_mu = p->unit_mu;
-    prm.chunk_map = p->chunk_map;
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
@@ -1024,7 +1001,7 @@ int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
 }
 
 size_t smem_budget(const CorrParams& prm) {
-    return 1024 + prm.table_bytes + (size_t)prm.stages * kStageA + 1024 + (size_t)prm.raw_stages * kRawStageBytes;
+    return 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 + (size_t)prm.raw_stages * prm.conv_links * kRawRowBytes;
 }
 
 }  // namespace
@@ -1039,16 +1016,16 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->packed, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     CUtensorMap tm_in;
-    s = make_tmap_packed(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, p->cfg.dtype == PNCE_DTYPE_BF16);
+    s = make_tmap16(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, prm.split ? 64 : kBM,
+                    p->cfg.dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) return s;
-    const int64_t avail = (int64_t)kSmemLimit - 2048 - prm.table_bytes;
-    prm.stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_AB_STAGES", 12), avail / kStageA);
+    prm.stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_AB_STAGES", 8), (kSmemLimit - 2048) / prm.stage_bytes);
     if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the correlator pipeline");
     k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), static_cast<cudaStream_t>(stream)>>>(
-        tm_in, prm);
+        tm_in, p->tm_circ, prm);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;
@@ -1065,27 +1042,29 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->fused, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
-    const int64_t avail = (int64_t)kSmemLimit - 2048 - prm.table_bytes;
+    const int64_t avail = (int64_t)kSmemLimit - 2048;
     bool raw_ok = ((size_t)prm.samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
     if (env_int("PNCE_TUNE_FUSED_MODE", kModeFusedTma) == kModeFusedLdg) raw_ok = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (raw_ok) {
-        // f32 rows TMA-staged in shared memory (default): raw ring + A ring
-        prm.stages = std::max(2, env_int("PNCE_TUNE_AB_STAGES", 4));
-        prm.raw_stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_RAW_STAGES", 6),
-                                                (avail - (int64_t)prm.stages * kStageA) / kRawStageBytes);
+        // f32 rows TMA-staged in shared memory (default): raw ring + A/B ring
+        const int64_t raw_bytes = (int64_t)prm.conv_links * kRawRowBytes;
+        prm.stages = std::max(2, env_int("PNCE_TUNE_AB_STAGES", 3));
+        prm.raw_stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_RAW_STAGES", 8),
+                                                (avail - (int64_t)prm.stages * prm.stage_bytes) / raw_bytes);
         if (prm.raw_stages < 2) {
             prm.stages = 2;
-            prm.raw_stages = (int)std::min<int64_t>(6, (avail - 2 * (int64_t)kStageA) / kRawStageBytes);
+            prm.raw_stages = (int)std::min<int64_t>(8, (avail - 2 * (int64_t)prm.stage_bytes) / raw_bytes);
         }
         if (prm.raw_stages < 1) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         CUtensorMap tm_raw;
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)prm.samples * 2, (uint64_t)(prm.total_rows / 2));
+        s = make_tmap_raw(&tm_raw, iq, (uint64_t)prm.samples * 2, (uint64_t)(prm.total_rows / 2),
+                          (uint32_t)prm.conv_links);
         if (s != PNCE_OK) return s;
-        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(tm_raw, prm);
+        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(tm_raw, p->tm_circ, prm);
 #ifdef PNCE_DIAG_TRACE
         if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
             static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
@@ -1098,11 +1077,9 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         }
 #endif
     } else {
-        prm.stages = (int)std::min<int64_t>(12, avail / kStageA);
+        prm.stages = (int)std::min<int64_t>(8, avail / prm.stage_bytes);
         if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
-        CUtensorMap dummy;
-        std::memset(&dummy, 0, sizeof(dummy));
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(dummy, prm);
+        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(p->tm_circ, p->tm_circ, prm);
     }
     g_launches++;
     CUDA_TRY(cudaGetLastError());

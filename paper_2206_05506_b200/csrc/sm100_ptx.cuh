@@ -324,4 +324,38 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
 }
 
+
+// TMA 2-D tile load multicast to every CTA in `mask` (same smem/barrier offsets in each).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t x, int32_t y,
+                                               uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%4, %5}], [%2], %3, %6;"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "h"(mask),
+          "r"(x), "r"(y), "l"(policy)
+        : "memory");
+}
+
+// Bulk copy of `bytes` from this CTA's shared memory to another CTA's shared memory
+// (shared::cluster addresses); completion is counted on the destination's mbarrier.
+__device__ __forceinline__ void bulk_copy_s2s(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                              uint32_t mbar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst_cluster), "r"(smem_u32(src)), "r"(bytes), "r"(mbar_cluster)
+        : "memory");
+}
+
+// Commit prior MMAs of this thread to the barrier at the same offset in the CTAs of `mask`.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+// Named barrier over `count` threads.
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 }  // namespace pnce
