@@ -2,35 +2,32 @@
 //
 // Hot path (reference: pnce/experiments.py:176-208 process_frames ->
 // pnce/estimator.py:68-86 correlate_rows):
-//   K1  k_lfsr / k_build_circulant : generate_mseq (pn.py:109-138) on the device and the
-//       stacked lag-window rows C[j*L+l, k] = chip[(k - s_j - l) mod M]
-//       (batched_lag_rows, estimator.py:62-65,114-117) as a 16-bit K-major operand.
-//   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the received
-//       f32 (I,Q) samples into 16-bit rows (frame, batch, rx, re|im) x K.  Only used by
-//       the two-pass path; the fused K3 does this itself.
-//   K3  k_correlate : tcgen05 UMMA   D[rows, lags] = X[rows, K] . C[lags, K]^T
-//       (both real GEMMs of estimator.py:77-80 in one contraction: Re and Im are separate
-//       rows of X).  Two CTAs of a cluster share one 128-row sample tile X (converted once,
-//       copied to the peer over DSMEM / TMA-multicast) and each accumulates half of the lag
-//       columns in its own double-buffered TMEM, so the epilogue of one tile overlaps the
-//       MMAs of the next.
-//   K4  fused into K3's epilogue: x 1/M, Re/Im pairing, per-transmitter window demux into
-//       taps[f, r, t, l] (experiments.py:206-207) and optional sum|e|, sum|e|^2 and
-//       non-finite count vs. truth (metrics.py:19-25 + the north-star MSE).
+//   K1  k_lfsr / k_build_circulant : generate_mseq (pn.py:109-138) on device and
+//       the stacked lag-window rows A[j*L+l, k] = chip[(k - s_j - l) mod M]
+//       (estimator.py:62-65,114-117) as an fp16/bf16 K-major operand.
+//   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the
+//       received f32 (I,Q) samples into rows (frame, batch, rx, re|im) x K.
+//   K3  k_correlate : tcgen05 UMMA  D^T[rows, R] = B^T[rows, K] . A^T[K, R]
+//       (both real GEMMs of estimator.py:77-80 in one contraction; the huge
+//       frame x rx x re/im axis is the UMMA M dimension), TMA-fed, warp-specialised,
+//       persistent, TMEM double-buffered accumulator.
+//   K4  (fused into K3's epilogue) x 1/M, Re/Im pairing, per-transmitter window
+//       demux into taps[f, r, t, l] (experiments.py:206-207) and optional
+//       sum|e|, sum|e|^2, non-finite count vs. truth (metrics.py:19-25 + MSE).
 #include <cuda.h>
-#include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
-#include <algorithm>
 #include <atomic>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
-#include <type_traits>
 #include <vector>
 
 #include "../../include/pnce_b200.h"
@@ -40,11 +37,10 @@ using namespace pnce;
 
 namespace {
 
-constexpr int kBM = 128;       // sample rows per UMMA (M)
+constexpr int kBM = 128;       // UMMA M (input rows per tile)
 constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
 constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
 constexpr int kSmemLimit = 227 * 1024;
-constexpr uint32_t kStageA = kBM * kBK * 2;  // 16 KB sample tile per stage
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -54,62 +50,54 @@ pnce_status_t fail(pnce_status_t code, const std::string& msg) {
     return code;
 }
 
-#define CUDA_TRY(expr)                                                                    \
-    do {                                                                                  \
-        cudaError_t e_ = (expr);                                                          \
-        if (e_ != cudaSuccess)                                                            \
+#define CUDA_TRY(expr)                                                                 \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess)                                                         \
             return fail(PNCE_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-}
-
-template <typename T>
-__device__ __forceinline__ T to16(float v) {
-    if constexpr (std::is_same<T, __half>::value) return __float2half_rn(v);
-    else return __float2bfloat16_rn(v);
-}
-
-// ------------------------------------------------------------------ K1: LFSR + circulant rows
+// ------------------------------------------------------------------ K1: LFSR
 // One thread runs the Fibonacci LFSR for one period (pn.py:115-137):
 // out = MSB, fb = parity(state & tap_mask), state = ((state << 1) | fb) & mask.
-__global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m, int* period_out) {
+__global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* chips, int m,
+                       int* period_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t mask = (1u << degree) - 1u;
     uint32_t s = state0;
     int n = 0;
     const int limit = 1 << degree;
     for (int i = 0; i < limit; ++i) {
-        const uint32_t bit = (s >> (degree - 1)) & 1u;
+        uint32_t bit = (s >> (degree - 1)) & 1u;
         if (n < m) chips[n] = bit ? -1.0f : 1.0f;
         ++n;
-        const uint32_t fb = __popc(s & tap_mask) & 1u;
+        uint32_t fb = __popc(s & tap_mask) & 1u;
         s = ((s << 1) | fb) & mask;
         if (s == state0) break;
     }
     *period_out = n;
 }
 
-// Stacked lag-window rows, K-major, zero padded: C[n, k] for n < rows_alloc, k < k_pad,
-// lag(n) = floor(M/N_b) * (n / L) + n % L  (shift_for_transmitter + window lag).
+// Stacked lag-window rows, K-major, zero padded: A[n, k] for n < rows_alloc, k < k_pad.
 template <typename T>
-__global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m, int k_pad, int r_total,
-                                  int rows_alloc, int l, int spacing) {
+__global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m,
+                                  int k_pad, int r_total, int rows_alloc, int l, int spacing, int repl) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t total = (int64_t)rows_alloc * k_pad;
+    int64_t total = (int64_t)rows_alloc * k_pad * repl;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-        const int n = (int)(idx / k_pad);
-        const int k = (int)(idx % k_pad);
+        int n = (int)((idx / k_pad) % rows_alloc);
+        int k = (int)(idx % k_pad);
         float v = 0.0f;
         if (n < r_total && k < m) {
-            const int lag = (spacing * (n / l) + (n % l)) % m;
+            int lag = (spacing * (n / l) + (n % l)) % m;  // shift_for_transmitter + window lag
             int ci = k - lag;
             if (ci < 0) ci += m;
             v = chips[ci];
         }
-        a[idx] = to16<T>(v);
+        if constexpr (sizeof(T) == 2 && std::is_same<T, __half>::value)
+            a[idx] = __float2half_rn(v);
+        else
+            a[idx] = __float2bfloat16_rn(v);
     }
 }
 
@@ -118,58 +106,68 @@ __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict
 // row q (q = (f*nb + b)*n_r + r), write 8 quantised Re to packed row 2q and
 // 8 Im to row 2q+1 (16 B each); zero beyond M.
 template <typename T>
-__global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links, int samples, int c,
-                          int m, int k_pad) {
+__global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links,
+                          int samples, int c, int m, int k_pad) {
     const int chunks = k_pad >> 3;
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t total = n_links * chunks;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = idx / chunks;
-        const int k0 = (int)(idx - q * chunks) << 3;
+        const int ch = (int)(idx - q * chunks);
+        const int k0 = ch << 3;
         const float2* src = reinterpret_cast<const float2*>(iq) + q * samples + c + k0;
+        float re[8], im[8];
+        if (k0 + 8 <= m) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float2 v = __ldg(src + j);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
+                re[j] = v.x;
+                im[j] = v.y;
+            }
+        }
         uint4 pr, pi;
         T* hr = reinterpret_cast<T*>(&pr);
         T* hi = reinterpret_cast<T*>(&pi);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
-            hr[j] = to16<T>(v.x);
-            hi[j] = to16<T>(v.y);
+            if constexpr (std::is_same<T, __half>::value) {
+                hr[j] = __float2half_rn(re[j]);
+                hi[j] = __float2half_rn(im[j]);
+            } else {
+                hr[j] = __float2bfloat16_rn(re[j]);
+                hi[j] = __float2bfloat16_rn(im[j]);
+            }
         }
-        *reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0) = pr;
+        uint4* dst = reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0);
+        dst[0] = pr;
         *reinterpret_cast<uint4*>(out + (2 * q + 1) * (int64_t)k_pad + k0) = pi;
     }
 }
 
 // ------------------------------------------------------------------ K3+K4
-// Variants (template MODE):
-//   kModePacked   : sample rows = the packed 16-bit operand of K2 (TMA, multicast to the pair);
-//   kModeFusedTma : sample rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
+// Correlation kernel, one CTA pair (cluster 2x1, tcgen05 cta_group::2) per 256 input
+// rows.  Variants (template MODE):
+//   kModePacked   : rows = the packed 16-bit operand of K2, TMA-loaded;
+//   kModeFusedTma : rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
 //                   converted (remove_cp + de-interleave + fp16/bf16) by converter warps
 //                   straight into the 128B-swizzled UMMA A stage -- K2 fused away;
-//   kModeFusedLdg : as above, converters LDG the f32 rows (fallback for row strides that
-//                   are not 16-byte multiples).
-// Pair split (CorrParams::split):
-//   1 (lags > 256): both CTAs of the cluster work on the SAME 128-row tile; each converts
-//     half of its 64 links and bulk-copies them to the peer, each accumulates half of the
-//     tile's lag columns;
-//   0 (lags <= 256): each CTA owns its own 128 rows and all lag columns (no sharing).
-// Warp roles (16 warps):
-//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer      2 raw-row TMA producer
-//   3 spare                                          4-11 converters   12-15 epilogue
+//   kModeFusedLdg : as above but converters LDG the f32 rows (fallback for row strides
+//                   that are not 16-byte multiples).
+// Warp roles (16 warps, both CTAs unless noted):
+//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader) / arrive forwarder (peer)
+//   2 raw-row TMA producer (FusedTma)                3 spare
+//   4-7 converters (fused)                           8-15 epilogue (2 warps per TMEM lane quarter)
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
-constexpr int kWarps = 16;
-constexpr int kThreadsK3 = kWarps * 32;
-constexpr int kConvWarp0 = 4;
-constexpr int kConvWarps = 8;
-constexpr int kEpiWarp0 = 12;
-constexpr int kEpiWarps = 4;
-constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
-constexpr uint32_t kRawRowBytes = kRawRowFloats * 4;
-constexpr int kConvBarId = 1;               // named barrier of the converter warps
 
 #ifdef PNCE_DIAG_TRACE
-// Diagnostic timeline (globaltimer ns) for the first two CTAs: [cta][slot][index].
+// Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
 constexpr int kTraceSlots = 16, kTraceMax = 512;
 __device__ long long g_trace[2 * kTraceSlots * kTraceMax];
 __device__ __forceinline__ long long gtimer() {
@@ -177,31 +175,42 @@ __device__ __forceinline__ long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TRACE(slot, idx)                                                                  \
-    do {                                                                                  \
-        if (blockIdx.x < 2 && (idx) < kTraceMax)                                          \
-            g_trace[(blockIdx.x * kTraceSlots + (slot)) * kTraceMax + (idx)] = gtimer(); \
+#define TRACE(slot, idx)                                                                   \
+    do {                                                                                   \
+        if (blockIdx.x < 2 && (idx) < kTraceMax)                                           \
+            g_trace[(blockIdx.x * kTraceSlots + (slot)) * kTraceMax + (idx)] = gtimer();  \
     } while (0)
 #else
 #define TRACE(slot, idx) \
     do {                 \
     } while (0)
 #endif
+constexpr int kWarps = 16;
+constexpr int kThreadsK3 = kWarps * 32;
+constexpr int kConvWarp0 = 4;
+constexpr int kConvWarps = 8;
+constexpr int kEpiWarp0 = 12;
+constexpr int kEpiWarps = 4;
+constexpr int kLinksPerTile = kBM / 2;                                        // 64 (re, im) row pairs
+constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
+constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
+constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;         // 64 links: 33 KB
 
 struct CorrParams {
     int64_t total_rows;  // n_frames * n_batches * n_r * 2
-    int32_t split;       // 1: pair shares a 128-row tile and splits its lag columns
-    int32_t m_tiles;     // pair tiles along the rows
-    int32_t n_groups;    // lag-column groups per tile
-    int32_t gc;          // accumulator columns per CTA per group (= n_mma * nm)
-    int32_t n_mma;       // MMAs per k-step, N = nm each
+    int32_t m_tiles;     // 256-row tiles (one per CTA pair)
+    int32_t n_groups;    // lag-row groups
+    int32_t g_cols;      // accumulator columns per group (= sum of the MMAs' N)
+    int32_t n_mma;       // MMAs per k-step (1 or 2), each N = nm
     int32_t nm;
-    int32_t acc_stages;  // TMEM accumulator buffers
+    int32_t acc_stages;  // TMEM accumulator buffers (2 if 2*g_cols <= 512)
     int32_t k_blocks;
-    int32_t stages;      // A+B stages
+    int32_t stages;
     int32_t raw_stages;  // FusedTma: f32 staging ring depth
-    int32_t conv_links;  // links converted per CTA per tile (32 split / 64 otherwise)
+    int32_t circ_repl;   // circulant replicas
+    int32_t circ_rows;   // rows per replica
     uint32_t stage_bytes;
+    uint32_t tx_bytes;   // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
@@ -219,9 +228,13 @@ struct ConvTask {
     float re[8], im[8];
 };
 
-__device__ __forceinline__ void conv_load(const CorrParams& p, int64_t q, int kb, int chunk, ConvTask& t) {
+__device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, int kb, int task, ConvTask& t) {
+    const int link_local = task >> 3;
+    const int chunk = task & 7;
+    const int64_t q = link0 + link_local;
     const int k0 = kb * kBK + chunk * 8;
-    const bool ok = q < (p.total_rows >> 1);
+    const int64_t total_links = p.total_rows >> 1;
+    const bool ok = q < total_links;
     const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -245,7 +258,10 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row)
     return base + row * 128 + ((((byte_in_row >> 4) ^ (row & 7))) << 4) + (byte_in_row & 15);
 }
 
-__device__ __forceinline__ void conv_store(uint32_t sa, int row_re, int chunk, const ConvTask& t, int bf16) {
+__device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask& t, int bf16) {
+    const int link_local = task >> 3;
+    const int chunk = task & 7;
+    const int row_re = 2 * link_local, row_im = row_re + 1;
     uint4 vr, vi;
     vr.x = pack2(t.re[0], t.re[1], bf16);
     vr.y = pack2(t.re[2], t.re[3], bf16);
@@ -256,14 +272,14 @@ __device__ __forceinline__ void conv_store(uint32_t sa, int row_re, int chunk, c
     vi.z = pack2(t.im[4], t.im[5], bf16);
     vi.w = pack2(t.im[6], t.im[7], bf16);
     st_shared_v4(swz(sa, row_re, chunk * 16), vr);
-    st_shared_v4(swz(sa, row_re + 1, chunk * 16), vi);
+    st_shared_v4(swz(sa, row_im, chunk * 16), vi);
 }
 
 // Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
-// Re/Im pairing: the even lane (Re row) keeps columns 0..7, the odd lane (Im row) 8..15.
 __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok,
-                                          int n_first, int n_valid, int64_t out_base, float& s_abs, float& s_sq,
-                                          float& s_bad) {
+                                          int n_first, int n_valid, int64_t out_base, float& s_abs,
+                                          float& s_sq, float& s_bad) {
+    // Re/Im pairing: the even lane keeps columns 0..7, the odd lane columns 8..15.
     float x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -277,6 +293,11 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
         o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
     }
+    if (p.stats != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
+    }
     const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
 #ifdef PNCE_DIAG_NO_STORE
     if (o[0] == 12345.678f) p.taps[g] = o[1];  // keep the work, drop the stores
@@ -286,11 +307,6 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         float* dst = p.taps + 2 * g;
         st_global_v8(dst, *reinterpret_cast<const float(*)[8]>(&o[0]));
         st_global_v8(dst + 8, *reinterpret_cast<const float(*)[8]>(&o[8]));
-        if (p.stats != nullptr) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (!(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
-        }
         if (p.truth != nullptr) {
             float h[16];
             ld_global_nc_v8(p.truth + 2 * g, *reinterpret_cast<float(*)[8]>(&h[0]));
@@ -310,7 +326,6 @@ __device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v
         for (int i = 0; i < 8; ++i) {
             if (n_first + i < n_valid) {
                 taps[g + i] = make_float2(o[2 * i], o[2 * i + 1]);
-                if (p.stats != nullptr && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
                 if (truth != nullptr) {
                     const float2 h = __ldg(truth + g + i);
                     const float dx = o[2 * i] - h.x, dy = o[2 * i + 1] - h.y;
@@ -330,8 +345,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     constexpr bool FUSED = MODE != kModePacked;
     constexpr bool RAW = MODE == kModeFusedTma;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // [A+B stages][1 KB barrier block][raw f32 stages]
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    // [A/B stages][1 KB barrier block][raw f32 stages]
     const int S = p.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
     uint64_t* empty = full + S;
@@ -341,42 +357,36 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
     uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
-    const uint32_t raw_stage_bytes = (uint32_t)p.conv_links * kRawRowBytes;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    const uint32_t peer = rank ^ 1u;
-    const bool split = p.split != 0;
-    const uint16_t pair_mask = 3;
-    // bytes of the half sample tile each CTA converts and ships to its peer (split mode)
-    const uint32_t half_a = kStageA / 2;
+    const bool leader = rank == 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            // full: the producer's expect_tx arrive (+ the converter group's arrive when fused);
-            //       the peer's TMA-multicast / bulk-copied half tile lands as transaction bytes.
-            // empty: released by the MMA of every CTA that reads this stage's sample tile.
-            mbar_init(&full[s], FUSED ? 2 : 1);
-            mbar_init(&empty[s], split ? 2 : 1);
+            // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
+            // bytes and converter arrives land on the leader's barrier).
+            mbar_init(&full[s], FUSED ? 1 + 2 * kConvWarps : 1);
+            mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiWarps);
+            mbar_init(&tempty[a], 2 * kEpiWarps);
         }
         if (RAW) {
             for (int s = 0; s < p.raw_stages; ++s) {
                 mbar_init(&raw_full[s], 1);
-                mbar_init(&raw_empty[s], 1);
+                mbar_init(&raw_empty[s], kConvWarps);
             }
         }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        if (MODE != kModeFusedLdg) tma_prefetch(&tm_in);
+        if (!FUSED || RAW) tma_prefetch(&tm_in);
         tma_prefetch(&tm_circ);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+    if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
@@ -387,20 +397,15 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int total_tiles = p.m_tiles * p.n_groups;
     const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
-    // first sample row of this CTA's MMA tile, and first link this CTA converts
-    auto tile_row0 = [&](int mt) -> int64_t {
-        return split ? (int64_t)mt * kBM : (int64_t)mt * 2 * kBM + (int64_t)rank * kBM;
-    };
-    auto conv_link0 = [&](int mt) -> int64_t { return tile_row0(mt) / 2 + (split ? (int64_t)rank * 32 : 0); };
-    // accumulator columns of this CTA in group g
-    auto col0 = [&](int g) -> int { return split ? (2 * g + (int)rank) * p.gc : g * p.gc; };
+    const uint32_t a_bytes = kBM * kBK * 2;
+    const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ===== TMA producer: circulant rows (+ packed sample rows)
+            // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
             const uint64_t pol_in = policy_evict_first();
             const uint64_t pol_circ = policy_evict_last();
-            const uint32_t b_bytes = (uint32_t)p.gc * kBK * 2;
+            const int circ_row0 = (cid % p.circ_repl) * p.circ_rows;
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
@@ -411,62 +416,58 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
                 TRACE(0, j);
                 uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
-                uint8_t* sb = sa + kStageA;
-                // this CTA receives: its B rows, plus (fused split) the peer's half tile, or
-                // (packed) the whole tile (own TMA + peer multicast in split mode)
-                const uint32_t tx = b_bytes + (FUSED ? (split ? half_a : 0u) : kStageA);
-                mbar_arrive_expect_tx(&full[stage], tx);
-                if (!FUSED) {
-                    if (split)
-                        tma_load_2d_mc(sa + rank * half_a, &tm_in, &full[stage], kb * kBK,
-                                       (int)(tile_row0(mt) + rank * 64), pair_mask, pol_in);
-                    else
-                        tma_load_2d(sa, &tm_in, &full[stage], kb * kBK, (int)tile_row0(mt), pol_in);
-                }
+                uint8_t* sb = sa + a_bytes;
+                const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
+                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
+                if (!FUSED)
+                    tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
                 for (int jj = 0; jj < p.n_mma; ++jj)
-                    tma_load_2d(sb + (size_t)jj * p.nm * kBK * 2, &tm_circ, &full[stage], kb * kBK,
-                                col0(g) + jj * p.nm, pol_circ);
+                    tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
+                                     circ_row0 + g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ===== MMA issuer (single thread): cta_group::1, M = 128, N = nm
+        if (leader && lane == 0) {
+            // ===== MMA issuer (leader CTA, single thread) for the whole pair
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int ti = 0; ti < my_tiles; ++ti) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 TRACE(1, ti);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.gc);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const int j = ti * p.k_blocks + kb;
                     const int stage = j % S;
-                    mbar_wait(&full[stage], (uint32_t)(j / S) & 1u);
+                    const uint32_t phase = (uint32_t)(j / S) & 1u;
+#ifndef PNCE_DIAG_NO_FULLWAIT
+                    mbar_wait(&full[stage], phase);
+#else
+                    (void)phase;
+#endif
                     TRACE(2, j);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-                    const uint32_t sb = sa + kStageA;
+                    const uint32_t sb = sa + a_bytes;
 #pragma unroll
                     for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
                         for (int jj = 0; jj < p.n_mma; ++jj) {
-                            const uint64_t bd = make_sdesc(sb + (uint32_t)(jj * p.nm * kBK * 2) + ks * 32, 16, 1024, 2);
-                            umma_f16_ss(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
+                            const uint64_t bd = make_sdesc(sb + jj * b_half_bytes + ks * 32, 16, 1024, 2);
+                            umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
                         }
                     }
-                    // the stage's sample tile is read by both CTAs in split mode: free it in both
-                    if (split) umma_commit_mc(&empty[stage], pair_mask);
-                    else umma_commit(&empty[stage]);
+                    umma_commit_pair(&empty[stage]);
                     TRACE(3, j);
                 }
-                umma_commit(&tfull[acc]);
+                umma_commit_pair(&tfull[acc]);
                 if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else if (warp == 2) {
         if (RAW && lane == 0) {
-            // ===== raw-row producer: TMA the f32 (I,Q) rows of the links this CTA converts
-            // for one K-block (64 samples x 8 B + slack per link) into the staging ring.
+            // ===== raw-row producer: TMA the f32 (I,Q) rows of this CTA's 64 links for one
+            // K-block (64 links x 64 samples x 8 B = 32 KB) into the staging ring.
             const uint64_t pol = policy_evict_first();
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
@@ -479,97 +480,90 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 mbar_arrive(&raw_full[rs]);
                 (void)pol; (void)mt; (void)kb;
 #else
-                mbar_arrive_expect_tx(&raw_full[rs], raw_stage_bytes);
+                mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
                 // box start rounded down to a 16-byte boundary; converters skip the slack
-                tma_load_2d(raw_base + (size_t)rs * raw_stage_bytes, &tm_in, &raw_full[rs],
-                            (2 * (p.c + kb * kBK)) & ~3, (int)conv_link0(mt), pol);
+                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs],
+                            (2 * (p.c + kb * kBK)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile, pol);
 #endif
             }
         }
     } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
         if (FUSED) {
-            // ===== converters: this CTA's links -> rows (2*link, 2*link+1) of the A stage;
-            // in split mode these are rows [64*rank, 64*rank+64) and are bulk-copied to the peer.
             const int cw = warp - kConvWarp0;
-            const bool elected = cw == 0 && lane == 0;
-            const int row_base = split ? 64 * (int)rank : 0;
             for (int j = 0; j < jobs; ++j) {
                 const int ti = j / p.k_blocks;
                 const int kb = j - ti * p.k_blocks;
                 const int stage = j % S;
-                uint8_t* sa_ptr = smem + (size_t)stage * p.stage_bytes;
-                const uint32_t sa = smem_u32(sa_ptr);
-                int rs = 0;
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
                 if (RAW) {
-                    // staged rows -> A stage.  Warp w converts links w, w+8, ...; lane l handles
-                    // samples 2l, 2l+1 (one conflict-free LDS of the staged row, two STS.32).
-                    rs = j % p.raw_stages;
+                    // staged f32 rows -> A stage.  Warp w converts links w, w+4, ...; lane l
+                    // handles samples 2l, 2l+1 (one conflict-free LDS.128 of the 512 B row,
+                    // two STS.32 into the Re / Im rows).
+                    const int rs = j % p.raw_stages;
                     mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
-                    if (elected) TRACE(7, j);
+                    if (cw == 0 && lane == 0) TRACE(7, j);
                     mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
-                    if (elected) TRACE(8, j);
+                    if (cw == 0 && lane == 0) TRACE(8, j);
                     const int slack = (2 * (p.c + kb * kBK)) & 3;  // 0 or 2 floats
-                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * raw_stage_bytes) + slack * 4 + lane * 16;
+                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * kRawStageBytes) + slack * 4 + lane * 16;
                     const int k = kb * kBK + 2 * lane;
                     const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
 #ifndef PNCE_DIAG_NO_CONV
 #pragma unroll 4
-                    for (int i = cw; i < p.conv_links; i += kConvWarps) {
-                        const uint32_t src = raw + i * kRawRowBytes;
+                    for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
+                        const int link_local = cw + kConvWarps * i;
                         float4 v;
                         if (slack == 0) {
-                            v = ld_shared_v4f(src);
+                            v = ld_shared_v4f(raw + link_local * (kRawRowFloats * 4));
                         } else {
-                            const float2 a = ld_shared_v2f(src);
-                            const float2 b = ld_shared_v2f(src + 8);
+                            const float2 a = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4));
+                            const float2 b = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4) + 8);
                             v = make_float4(a.x, a.y, b.x, b.y);
                         }
                         if (!ok0) { v.x = 0.f; v.y = 0.f; }
                         if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                        const int row = row_base + 2 * i;
-                        st_shared_u32(swz(sa, row, lane * 4), pack2(v.x, v.z, p.bf16));
-                        st_shared_u32(swz(sa, row + 1, lane * 4), pack2(v.y, v.w, p.bf16));
+                        st_shared_u32(swz(sa, 2 * link_local, lane * 4), pack2(v.x, v.z, p.bf16));
+                        st_shared_u32(swz(sa, 2 * link_local + 1, lane * 4), pack2(v.y, v.w, p.bf16));
                     }
 #else
                     (void)raw; (void)ok0; (void)ok1;
 #endif
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        // proxy fence above completed this warp's STS; plain (CTA-scope
+                        // release) arrive on the leader's barrier, no GPU-scope membar
+                        mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                        mbar_arrive(&raw_empty[rs]);
+                        if (cw == 0) TRACE(9, j);
+                    }
                 } else {
-                    // LDG fallback: (link, 8-sample chunk) tasks
+                    // LDG fallback: 4 tasks (link, 8-sample chunk) per thread
                     const int mt = (cid + ti * n_clusters) / p.n_groups;
-                    const int64_t link0 = conv_link0(mt);
+                    const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
                     const int ct = cw * 32 + lane;
-                    const int tasks = p.conv_links * 8;
-                    ConvTask buf[2];
-                    const int n_my = (tasks - ct + kConvWarps * 32 - 1) / (kConvWarps * 32);
+                    ConvTask buf[kTasksPerThread];
 #pragma unroll
-                    for (int i = 0; i < 2; ++i)
-                        if (i < n_my) conv_load(p, link0 + ((ct + i * kConvWarps * 32) >> 3), kb,
-                                                (ct + i * kConvWarps * 32) & 7, buf[i]);
+                    for (int i = 0; i < kTasksPerThread; ++i)
+                        conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
                     mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
 #pragma unroll
-                    for (int i = 0; i < 2; ++i) {
-                        const int t = ct + i * kConvWarps * 32;
-                        if (i < n_my) conv_store(sa, row_base + 2 * (t >> 3), t & 7, buf[i], p.bf16);
-                    }
-                }
-                // all converter warps' STS -> async proxy; then one thread publishes
-                fence_proxy_async_smem();
-                named_bar_sync(kConvBarId, kConvWarps * 32);
-                if (elected) {
-                    if (split) {
-                        // ship our half tile to the peer; its bytes complete the peer's full barrier
-                        bulk_copy_s2s(mapa_shared(sa + (uint32_t)row_base * 128, peer), sa_ptr + row_base * 128, half_a,
-                                      mapa_shared(smem_u32(&full[stage]), peer));
-                    }
-                    mbar_arrive(&full[stage]);
-                    if (RAW) mbar_arrive(&raw_empty[rs]);
-                    TRACE(9, j);
+                    for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                 }
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ===== epilogue: TMEM lane quarter = warp % 4; all of this CTA's columns
+        // ===== epilogue (both CTAs): TMEM lane quarter = warp % 4, column slice = (warp-first)/4
+        constexpr int kSlices = kEpiWarps / 4;
         const int quarter = warp & 3;
+        const int half = (warp - kEpiWarp0) >> 2;
+        const int cph = ((p.g_cols + kSlices - 1) / kSlices + 15) / 16 * 16;
+        const int c_begin = min(p.g_cols, half * cph);
+        const int c_end = min(p.g_cols, c_begin + cph);
+        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int ti = 0; ti < my_tiles; ++ti) {
@@ -580,7 +574,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
             tc_fence_after();
 
-            const int64_t row = tile_row0(mt) + quarter * 32 + lane;
+            const int64_t row = (int64_t)mt * 2 * kBM + (int64_t)rank * kBM + quarter * 32 + lane;
             const bool row_ok = row < p.total_rows;
             const bool odd = (lane & 1) != 0;
             const int64_t link = row >> 1;
@@ -593,28 +587,29 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
             float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
 
-            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.gc);
-            const int n0 = col0(g) + (odd ? 8 : 0);
+            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.g_cols);
+            const int n_tile0 = g * p.g_cols;
             // 32-column chunks (two 16-column slices each); the next chunk's TMEM load is
             // in flight while the current one is paired, scaled and stored.
             uint32_t va[32], vb[32];
-            int c0 = 0;
-            const int c_end = p.gc;
+            int c0 = c_begin;
             if (c0 + 32 <= c_end) {
                 tmem_ld32_nowait(t_row + c0, va);
                 tmem_wait_ld();
                 while (true) {
                     const bool more = c0 + 64 <= c_end;
                     if (more) tmem_ld32_nowait(t_row + c0 + 32, vb);
-                    epi_slice(p, va, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, va + 16, odd, row_ok, n0 + c0 + 16, n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, va + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
+                              s_sq, s_bad);
                     c0 += 32;
                     if (!more) break;
                     tmem_wait_ld();
                     const bool more2 = c0 + 64 <= c_end;
                     if (more2) tmem_ld32_nowait(t_row + c0 + 32, va);
-                    epi_slice(p, vb, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, vb + 16, odd, row_ok, n0 + c0 + 16, n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+                    epi_slice(p, vb + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
+                              s_sq, s_bad);
                     c0 += 32;
                     if (!more2) break;
                     tmem_wait_ld();
@@ -623,13 +618,14 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (c0 < c_end) {  // 16-column remainder
                 tmem_ld16_nowait(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(va));
                 tmem_wait_ld();
-                epi_slice(p, va, odd, row_ok, n0 + c0, n_valid, out_base, s_abs, s_sq, s_bad);
+                epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
             }
-            // accumulator buffer drained -> hand it back to this CTA's MMA thread
+            // this warp's share of the accumulator is drained -> tell the leader's MMA warp
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
             if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
+            if (lane == 0 && warp == kEpiWarp0 + kEpiWarps - 1) TRACE(12, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
 
             if (p.stats != nullptr) {
@@ -665,10 +661,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 
     __syncwarp();
     tc_fence_before();
-    cluster_sync_all();  // the peer may still be writing our smem / arriving on our barriers
+    cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, p.tmem_cols);
+        tmem_dealloc_pair(tmem_base, p.tmem_cols);
     }
 }
 
@@ -679,7 +675,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     std::call_once(once, [] {
         void* ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     });
@@ -687,31 +684,31 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2-D row-major [rows][cols] 16-bit tensor, box [box_rows][64], 128B swizzle.
-pnce_status_t make_tmap16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
-                          int bf16) {
+pnce_status_t make_tmap(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                        uint32_t box_rows, int bf16) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 2};
     cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return PNCE_OK;
 }
 
-// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [links_box][132 floats]
-// (one K-block of 64 (I,Q) samples + 16 B slack so the box start can be rounded down to
-// a 16-byte boundary), no swizzle.
-pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows,
-                            uint32_t links_box) {
+// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][132 floats]
+// (one K-block of 64 (I,Q) samples for 64 links + 16 B slack so the box start can be
+// rounded down to a 16-byte boundary), no swizzle.
+pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {row_floats, rows};
     cuuint64_t strides[1] = {row_floats * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, links_box};
+    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, (cuuint32_t)kLinksPerTile};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -720,64 +717,60 @@ pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_fl
     return PNCE_OK;
 }
 
-// Lag-column tiling (shared by all K3 variants).
-struct Tiling {
-    int split;       // pair shares the sample tile, splits the lag columns
-    int n_groups;    // column groups per tile
-    int gc;          // accumulator columns per CTA per group
-    int n_mma, nm;   // MMAs per k-step and their N
-    int acc_stages;
-    int rows_needed; // circulant rows the tiling addresses
-    uint32_t tmem_cols;
-    uint32_t stage_bytes;
-};
-
-Tiling make_tiling(int r_total) {
-    Tiling t{};
-    const int r16 = (r_total + 15) / 16 * 16;
-    const int max_cta_cols = env_int("PNCE_TUNE_CTA_COLS", 256);
-    if (r16 <= max_cta_cols) {
-        t.split = 0;
-        t.n_groups = 1;
-        t.gc = r16;
-    } else {
-        t.split = 1;
-        t.n_groups = (r16 + 2 * max_cta_cols - 1) / (2 * max_cta_cols);
-        t.gc = ((r16 + 2 * t.n_groups - 1) / (2 * t.n_groups) + 15) / 16 * 16;
-    }
-    t.n_mma = (t.gc + 255) / 256;
-    t.nm = t.gc / t.n_mma;
-    if (t.nm * t.n_mma != t.gc || t.nm % 16 != 0) {  // keep N a multiple of 16
-        t.nm = (t.nm + 15) / 16 * 16;
-        t.gc = t.nm * t.n_mma;
-    }
-    t.acc_stages = (2 * t.gc <= 512) ? 2 : 1;
-    t.rows_needed = t.n_groups * t.gc * (t.split ? 2 : 1);
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(t.acc_stages * t.gc)) cols <<= 1;
-    t.tmem_cols = cols;
-    t.stage_bytes = kStageA + (uint32_t)t.gc * kBK * 2;
-    return t;
-}
-
 }  // namespace
+
+// Lag-row tiling of one K3 variant.
+struct Tiling {
+    int n_groups;    // lag-row groups per 256-row tile
+    int g_cols;      // accumulator columns per group
+    int n_mma;       // pair MMAs per k-step (N = nm each)
+    int nm;
+    int acc_stages;  // TMEM accumulator buffers
+    int stages;      // smem pipeline depth
+    uint32_t stage_bytes;
+    uint32_t tmem_cols;
+    CUtensorMap tm_circ;  // circulant rows, box = nm/2 rows x 64 K
+};
 
 struct pnce_plan {
     pnce_cfg_t cfg;
     int n_batches;
     int r_total;     // N_b * L
     int k_pad;       // roundup(M, 64)
+    int rows_alloc;  // circulant rows per replica (>= both tilings' coverage)
+    int repl;        // circulant replicas: CTA pairs spread their B loads over replicas so
+                     // the whole grid does not hammer the same L2 lines in lock-step
     int num_sms;
-    Tiling tiling;
-    int rows_alloc;  // circulant rows allocated
+    Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
+    Tiling packed;   // packed operand in: groups of <= 256 cols, double-buffered accumulator
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
-    CUtensorMap tm_circ;
 };
+
+static void make_tiling(Tiling& t, int r_total, int max_group) {
+    const int r16 = (r_total + 15) / 16 * 16;
+    t.n_groups = (r16 + max_group - 1) / max_group;
+    int g = ((r16 + t.n_groups - 1) / t.n_groups + 15) / 16 * 16;
+    if (g > 256) {
+        g = (g + 31) / 32 * 32;
+        t.n_mma = 2;
+    } else {
+        t.n_mma = 1;
+    }
+    t.g_cols = g;
+    t.nm = g / t.n_mma;
+    t.acc_stages = (2 * g <= 512) ? 2 : 1;
+    t.stage_bytes = (uint32_t)(kBM * kBK * 2 + (g / 2) * kBK * 2);
+    int stages = (int)((kSmemLimit - 2048) / t.stage_bytes);
+    t.stages = stages > 8 ? 8 : stages;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(t.acc_stages * g)) cols <<= 1;
+    t.tmem_cols = cols;
+}
 
 extern "C" {
 
-int32_t pnce_version(void) { return 300; }
+int32_t pnce_version(void) { return 100; }
 
 const char* pnce_last_error(void) { return g_err.c_str(); }
 
@@ -785,13 +778,16 @@ int64_t pnce_kernel_launches(void) { return g_launches.load(); }
 
 pnce_status_t pnce_config_check(const pnce_cfg_t* cfg) {
     if (!cfg) return fail(PNCE_ERR_INVALID_CONFIG, "null config");
-    if (cfg->degree < 2 || cfg->degree > 16) return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
+    if (cfg->degree < 2 || cfg->degree > 16)
+        return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
     const uint32_t full = (1u << cfg->degree) - 1u;
     if (cfg->state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
     if (cfg->state > full) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
-    if (!(cfg->tap_mask & (1u << (cfg->degree - 1)))) return fail(PNCE_ERR_INVALID_SPEC, "tap set must include the degree");
+    if (!(cfg->tap_mask & (1u << (cfg->degree - 1))))
+        return fail(PNCE_ERR_INVALID_SPEC, "tap set must include the degree");
     if (cfg->tap_mask & ~full) return fail(PNCE_ERR_INVALID_SPEC, "tap outside [1, degree]");
-    if ((int64_t)cfg->m != (int64_t)full) return fail(PNCE_ERR_INVALID_CONFIG, "m must equal 2^degree - 1");
+    if ((int64_t)cfg->m != (int64_t)full)
+        return fail(PNCE_ERR_INVALID_CONFIG, "m must equal 2^degree - 1");
     if (cfg->n_t < 1 || cfg->n_r < 1) return fail(PNCE_ERR_INVALID_CONFIG, "n_t, n_r must be >= 1");
     if (!(1 <= cfg->l && cfg->l <= cfg->c && cfg->c <= cfg->m))
         return fail(PNCE_ERR_INVALID_CONFIG, "need 1 <= L <= C <= M");
@@ -810,8 +806,8 @@ pnce_status_t pnce_config_check(const pnce_cfg_t* cfg) {
     return PNCE_OK;
 }
 
-pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state, float* chips_dev, int32_t m,
-                                 void* stream) {
+pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t state, float* chips_dev,
+                                 int32_t m, void* stream) {
     if (degree < 2 || degree > 16) return fail(PNCE_ERR_INVALID_SPEC, "degree must be in [2, 16]");
     if (state == 0) return fail(PNCE_ERR_ZERO_STATE, "initial LFSR state must be nonzero");
     if (state >= (1u << degree)) return fail(PNCE_ERR_INVALID_SPEC, "state wider than degree bits");
@@ -828,8 +824,8 @@ pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t sta
     cudaFreeAsync(d_period, st);
     if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("k_lfsr: ") + cudaGetErrorString(e));
     if (period != m)
-        return fail(PNCE_ERR_NOT_MAXIMAL, "LFSR period " + std::to_string(period) + " != " + std::to_string(m) +
-                                              "; feedback polynomial is not primitive");
+        return fail(PNCE_ERR_NOT_MAXIMAL, "LFSR period " + std::to_string(period) + " != " +
+                                              std::to_string(m) + "; feedback polynomial is not primitive");
     return PNCE_OK;
 }
 
@@ -850,13 +846,19 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
     p->r_total = cfg->n_batch * cfg->l;
     p->k_pad = (cfg->m + kBK - 1) / kBK * kBK;
+    // Tuning knobs (diagnostics): maximum accumulator columns per lag-row group.
+    const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
+    const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
+    make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
+    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 256);
+    p->rows_alloc = std::max(p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols);
     p->num_sms = sms;
-    p->tiling = make_tiling(p->r_total);
-    p->rows_alloc = p->tiling.rows_needed;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
+    const char* rp = std::getenv("PNCE_TUNE_CIRC_REPL");
+    p->repl = std::max(1, std::min(64, rp ? std::atoi(rp) : 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2 * p->repl);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
@@ -867,14 +869,14 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         return s;
     }
     const int spacing = cfg->m / cfg->n_batch;
-    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad * p->repl;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     if (cfg->dtype == PNCE_DTYPE_BF16)
-        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad,
-                                                                  p->r_total, p->rows_alloc, cfg->l, spacing);
+        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
     else
-        k_build_circulant<__half><<<blocks, 256, 0, st>>>(p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total,
-                                                           p->rows_alloc, cfg->l, spacing);
+        k_build_circulant<__half><<<blocks, 256, 0, st>>>(
+            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
     g_launches++;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -882,7 +884,11 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
     }
-    s = make_tmap16(&p->tm_circ, p->circ, p->k_pad, p->rows_alloc, p->tiling.nm, cfg->dtype == PNCE_DTYPE_BF16);
+    const uint64_t circ_rows = (uint64_t)p->rows_alloc * p->repl;
+    s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
+    if (s == PNCE_OK)
+        s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
+                      cfg->dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
         return s;
@@ -890,7 +896,8 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(k_correlate<kModePacked>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        attr_err = cudaFuncSetAttribute(k_correlate<kModePacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kSmemLimit);
         if (attr_err == cudaSuccess)
             attr_err = cudaFuncSetAttribute(k_correlate<kModeFusedLdg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmemLimit);
@@ -927,7 +934,8 @@ size_t pnce_workspace_bytes(const pnce_plan_t* p, int64_t n_frames) {
     return (size_t)rows * p->k_pad * 2;
 }
 
-pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, int64_t n_frames, void* stream) {
+pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, int64_t n_frames,
+                           void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
@@ -938,7 +946,8 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     const int samples = c.c + c.m + c.l - 1;
     const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
     const int64_t work = links * (p->k_pad / 8);
-    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)p->num_sms * 16);
+    const int64_t want = (work + 255) / 256;
+    const int blocks = (int)(want < (int64_t)p->num_sms * 16 ? want : (int64_t)p->num_sms * 16);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (c.dtype == PNCE_DTYPE_BF16)
         k_pack_iq<__nv_bfloat16><<<blocks, 256, 0, st>>>(iq, (__nv_bfloat16*)packed, links, samples, c.c, c.m, p->k_pad);
@@ -949,34 +958,31 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     return PNCE_OK;
 }
 
-}  // extern "C"
-
-namespace {
-
-// Shared launch setup for all K3 variants.
-pnce_status_t fill_params(const pnce_plan_t* p, float* taps, const float* truth, double* stats, int64_t n_frames,
-                          CorrParams& prm) {
+// Shared launch setup for both K3 variants.
+static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fused, float* taps, const float* truth,
+                                 double* stats, int64_t n_frames, CorrParams& prm) {
     if ((reinterpret_cast<uintptr_t>(taps) & 7) || (truth && (reinterpret_cast<uintptr_t>(truth) & 7)))
         return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
     const pnce_cfg_t& c = p->cfg;
-    const Tiling& t = p->tiling;
     prm = CorrParams{};
     prm.total_rows = n_frames * p->n_batches * (int64_t)c.n_r * 2;
-    const int64_t tile_rows = t.split ? kBM : 2 * kBM;
-    const int64_t m_tiles = (prm.total_rows + tile_rows - 1) / tile_rows;
+    const int64_t m_tiles = (prm.total_rows + 2 * kBM - 1) / (2 * kBM);
     if (m_tiles * t.n_groups > INT32_MAX || prm.total_rows > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
-    prm.split = t.split;
     prm.m_tiles = (int32_t)m_tiles;
+    prm.circ_repl = p->repl;
+    prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
-    prm.gc = t.gc;
+    prm.g_cols = t.g_cols;
     prm.n_mma = t.n_mma;
     prm.nm = t.nm;
     prm.acc_stages = t.acc_stages;
     prm.k_blocks = p->k_pad / kBK;
-    prm.conv_links = t.split ? 32 : 64;
+    prm.stages = t.stages;
     prm.stage_bytes = t.stage_bytes;
-    prm.idesc = make_idesc_f16(kBM, t.nm, c.dtype == PNCE_DTYPE_BF16);
+    const uint32_t b_half = (uint32_t)(t.g_cols / 2) * kBK * 2;
+    prm.tx_bytes = 2 * (b_half + (fused ? 0u : (uint32_t)(kBM * kBK * 2)));
+    prm.idesc = make_idesc_f16(2 * kBM, t.nm, c.dtype == PNCE_DTYPE_BF16);
     prm.tmem_cols = t.tmem_cols;
     prm.n_r = c.n_r;
     prm.n_t = c.n_t;
@@ -994,38 +1000,28 @@ pnce_status_t fill_params(const pnce_plan_t* p, float* taps, const float* truth,
     return PNCE_OK;
 }
 
-int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
+static int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
     const int64_t tiles = (int64_t)prm.m_tiles * prm.n_groups;
     const int64_t pairs = std::min<int64_t>(tiles, p->num_sms / 2);
     return (int)(2 * std::max<int64_t>(pairs, 1));
 }
 
-size_t smem_budget(const CorrParams& prm) {
-    return 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 + (size_t)prm.raw_stages * prm.conv_links * kRawRowBytes;
-}
-
-}  // namespace
-
-extern "C" {
-
-pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth, double* stats,
-                             int64_t n_frames, void* stream) {
+pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
+                             double* stats, int64_t n_frames, void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
     if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, p->packed, false, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     CUtensorMap tm_in;
-    s = make_tmap16(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, prm.split ? 64 : kBM,
-                    p->cfg.dtype == PNCE_DTYPE_BF16);
+    s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) return s;
-    prm.stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_AB_STAGES", 8), (kSmemLimit - 2048) / prm.stage_bytes);
-    if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the correlator pipeline");
-    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), static_cast<cudaStream_t>(stream)>>>(
-        tm_in, p->tm_circ, prm);
+    const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
+    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, static_cast<cudaStream_t>(stream)>>>(
+        tm_in, p->packed.tm_circ, prm);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;
@@ -1042,29 +1038,30 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, p->fused, true, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
-    const int64_t avail = (int64_t)kSmemLimit - 2048;
-    bool raw_ok = ((size_t)prm.samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
-    if (env_int("PNCE_TUNE_FUSED_MODE", kModeFusedTma) == kModeFusedLdg) raw_ok = false;
+    const int samples = prm.samples;
+    const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
+    bool raw_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
+    if (fm && std::atoi(fm) == kModeFusedLdg) raw_ok = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (raw_ok) {
         // f32 rows TMA-staged in shared memory (default): raw ring + A/B ring
-        const int64_t raw_bytes = (int64_t)prm.conv_links * kRawRowBytes;
-        prm.stages = std::max(2, env_int("PNCE_TUNE_AB_STAGES", 3));
-        prm.raw_stages = (int)std::min<int64_t>(env_int("PNCE_TUNE_RAW_STAGES", 8),
-                                                (avail - (int64_t)prm.stages * prm.stage_bytes) / raw_bytes);
-        if (prm.raw_stages < 2) {
-            prm.stages = 2;
-            prm.raw_stages = (int)std::min<int64_t>(8, (avail - 2 * (int64_t)prm.stage_bytes) / raw_bytes);
-        }
-        if (prm.raw_stages < 1) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        const char* rs = std::getenv("PNCE_TUNE_RAW_STAGES");
+        prm.raw_stages = rs ? std::max(1, std::atoi(rs)) : 2;
+        const int64_t avail = (int64_t)kSmemLimit - 2048 - (int64_t)prm.raw_stages * kRawStageBytes;
+        int ab = (int)std::min<int64_t>(8, avail / (int64_t)prm.stage_bytes);
+        const char* as = std::getenv("PNCE_TUNE_AB_STAGES");
+        if (as) ab = std::min(ab, std::max(1, std::atoi(as)));
+        if (ab < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        prm.stages = ab;
         CUtensorMap tm_raw;
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)prm.samples * 2, (uint64_t)(prm.total_rows / 2),
-                          (uint32_t)prm.conv_links);
+        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)(prm.total_rows / 2));
         if (s != PNCE_OK) return s;
-        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(tm_raw, p->tm_circ, prm);
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
+                            (size_t)prm.raw_stages * kRawStageBytes;
+        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
 #ifdef PNCE_DIAG_TRACE
         if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
             static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
@@ -1077,9 +1074,10 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         }
 #endif
     } else {
-        prm.stages = (int)std::min<int64_t>(8, avail / prm.stage_bytes);
-        if (prm.stages < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem_budget(prm), st>>>(p->tm_circ, p->tm_circ, prm);
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
+        // tm_in is unused by the LDG-fused variant; pass the circulant map in its slot.
+        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(p->fused.tm_circ,
+                                                                                   p->fused.tm_circ, prm);
     }
     g_launches++;
     CUDA_TRY(cudaGetLastError());
