@@ -223,12 +223,11 @@ def run_gpu(args, rank, world):
 
     # --- resident synthetic input: a pool of distinct frame-sets tiled to F (> L2)
     pool_n = min(F, 64)
-    pool, _ = synth_iq_pool(corr, pool_n, w, seed=1234 + rank, dev=dev)
+    pool, h_pool = synth_iq_pool(corr, pool_n, w, seed=1234 + rank, dev=dev)
     iq = torch.empty(corr.iq_shape(F), dtype=torch.float32, device=dev)
     for s in range(0, F, pool_n):
         e = min(F, s + pool_n)
         iq[s:e].copy_(pool[:e - s])
-    del pool
     taps = torch.empty(corr.taps_shape(F), dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
     L = _lib.lib()
@@ -282,6 +281,16 @@ def run_gpu(args, rank, world):
                 traffic = per_frame * F if per_frame else None
         except Exception:
             traffic = None
+
+    # --- estimate quality on the synthetic pool: fused scoring + NCCL all-reduce of the
+    # per-rank error sums (the only collective of the path)
+    from paper_2206_05506_b200 import distributed as D
+    pool_stats = torch.zeros((pool_n, 4), dtype=torch.float64, device=dev)
+    corr.process(pool, truth=h_pool, out=taps[:pool_n], stats=pool_stats)
+    quality = D.global_metrics(pool_stats, w["n_r"] * w["n_t"] * w["l"], pool_n * world)
+    quality["mse_db"] = 10 * math.log10(quality["mse"]) if quality["mse"] > 0 else None
+    quality["frames"] = pool_n * world
+    del pool
 
     # --- GEMM-only leg (K3 on the pre-packed fp16 operand): the north-star tensor-% number
     gemm = None
@@ -362,6 +371,7 @@ def run_gpu(args, rank, world):
                                          "bytes": "f32 CP-stripped body in + complex64 taps out",
                                          "frames_per_launch": F}},
             "gemm_leg": gemm,
+            "estimate_quality": quality,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
