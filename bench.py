@@ -285,11 +285,18 @@ def run_gpu(args, rank, world):
     # --- estimate quality on the synthetic pool: fused scoring + NCCL all-reduce of the
     # per-rank error sums (the only collective of the path)
     from paper_2206_05506_b200 import distributed as D
-    pool_stats = torch.zeros((pool_n, 4), dtype=torch.float64, device=dev)
-    corr.process(pool, truth=h_pool, out=taps[:pool_n], stats=pool_stats)
-    quality = D.global_metrics(pool_stats, w["n_r"] * w["n_t"] * w["l"], pool_n * world)
-    quality["mse_db"] = 10 * math.log10(quality["mse"]) if quality["mse"] > 0 else None
-    quality["frames"] = pool_n * world
+    quality = None
+    if not args.no_quality:
+        pool_stats = torch.zeros((pool_n, 4), dtype=torch.float64, device=dev)
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record()
+        corr.process(pool, truth=h_pool, out=taps[:pool_n], stats=pool_stats)
+        q1.record()
+        torch.cuda.synchronize()
+        quality = D.global_metrics(pool_stats, w["n_r"] * w["n_t"] * w["l"], pool_n * world)
+        quality["mse_db"] = 10 * math.log10(quality["mse"]) if quality["mse"] > 0 else None
+        quality["frames"] = pool_n * world
+        quality["scored_us_per_frame"] = q0.elapsed_time(q1) * 1e3 / pool_n
     del pool
 
     # --- GEMM-only leg (K3 on the pre-packed fp16 operand): the north-star tensor-% number
@@ -390,6 +397,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gemm-leg", action="store_true")
+    ap.add_argument("--no-quality", action="store_true", help="skip the fused-scoring quality pass")
     ap.add_argument("--gemm-frames", type=int, default=4096)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)

@@ -94,7 +94,11 @@ pnce_status_t pnce_plan_destroy(pnce_plan_t* plan);
 /* Copy the plan's device-generated chips (float32 [m]) into dst_dev. */
 pnce_status_t pnce_plan_chips(const pnce_plan_t* plan, float* dst_dev, void* stream);
 
-/* Bytes of the packed 16-bit operand pnce_pack_iq writes for n_frames. */
+/* Bytes of the packed 16-bit operand pnce_pack_iq writes for n_frames.
+ * Packed layout: K_pad = roundup(m, 64) columns; links q = (f*n_batches + b)*n_r + r are
+ * grouped by 8 and each 16-row block holds the block's 8 Re rows then its 8 Im rows
+ * (Re of q at row 16*(q/8) + q%8, Im at 16*(q/8) + 8 + q%8); rows of padding links up to
+ * a multiple of 8, and columns >= m, are zero.  Rows = 16 * ceil(links / 8). */
 size_t pnce_workspace_bytes(const pnce_plan_t* plan, int64_t n_frames);
 
 /* K2 alone: CP removal (remove_cp, estimator.py:40-47) + de-interleave +

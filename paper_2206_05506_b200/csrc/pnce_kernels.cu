@@ -102,22 +102,30 @@ __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict
 }
 
 // ------------------------------------------------------------------ K2: pack
-// One thread per (link row q, 8-sample chunk c): read samples [C+8c, C+8c+8) of
-// row q (q = (f*nb + b)*n_r + r), write 8 quantised Re to packed row 2q and
-// 8 Im to row 2q+1 (16 B each); zero beyond M.
+// Packed-operand row order (shared with the fused converters): links are grouped by 8 and
+// each 16-row block holds the 8 Re rows then the 8 Im rows, so that the 16x256b TMEM load
+// of the epilogue hands one thread Re and Im of the same link (see k_correlate).
+__host__ __device__ __forceinline__ int64_t a_row(int64_t link, int im) {
+    return ((link >> 3) << 4) | ((int64_t)im << 3) | (link & 7);
+}
+
+// One thread per (link q, 8-sample chunk c): read samples [C+8c, C+8c+8) of link q
+// (q = (f*nb + b)*n_r + r), write 8 quantised Re to row a_row(q, 0) and 8 Im to
+// a_row(q, 1) (16 B each); zero beyond M and for the padding links up to a multiple of 8.
 template <typename T>
 __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int64_t n_links,
                           int samples, int c, int m, int k_pad) {
     const int chunks = k_pad >> 3;
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t total = n_links * chunks;
+    const int64_t padded = (n_links + 7) & ~int64_t(7);
+    const int64_t total = padded * chunks;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = idx / chunks;
         const int ch = (int)(idx - q * chunks);
         const int k0 = ch << 3;
-        const float2* src = reinterpret_cast<const float2*>(iq) + q * samples + c + k0;
         float re[8], im[8];
-        if (k0 + 8 <= m) {
+        if (q < n_links && k0 + 8 <= m) {
+            const float2* src = reinterpret_cast<const float2*>(iq) + q * samples + c + k0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 float2 v = __ldg(src + j);
@@ -125,9 +133,10 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
                 im[j] = v.y;
             }
         } else {
+            const float2* src = reinterpret_cast<const float2*>(iq) + (q < n_links ? q : 0) * samples + c + k0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                float2 v = (k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
+                float2 v = (q < n_links && k0 + j < m) ? __ldg(src + j) : make_float2(0.f, 0.f);
                 re[j] = v.x;
                 im[j] = v.y;
             }
@@ -145,25 +154,26 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
                 hi[j] = __float2bfloat16_rn(im[j]);
             }
         }
-        uint4* dst = reinterpret_cast<uint4*>(out + (2 * q) * (int64_t)k_pad + k0);
-        dst[0] = pr;
-        *reinterpret_cast<uint4*>(out + (2 * q + 1) * (int64_t)k_pad + k0) = pi;
+        *reinterpret_cast<uint4*>(out + a_row(q, 0) * k_pad + k0) = pr;
+        *reinterpret_cast<uint4*>(out + a_row(q, 1) * k_pad + k0) = pi;
     }
 }
 
 // ------------------------------------------------------------------ K3+K4
 // Correlation kernel, one CTA pair (cluster 2x1, tcgen05 cta_group::2) per 256 input
-// rows.  Variants (template MODE):
+// rows (128 links; each CTA owns 64 links = 128 A rows in the a_row order above).
+// Variants (template MODE):
 //   kModePacked   : rows = the packed 16-bit operand of K2, TMA-loaded;
-//   kModeFusedTma : rows = raw f32 (I,Q) frames, TMA-staged in shared memory and
-//                   converted (remove_cp + de-interleave + fp16/bf16) by converter warps
-//                   straight into the 128B-swizzled UMMA A stage -- K2 fused away;
-//   kModeFusedLdg : as above but converters LDG the f32 rows (fallback for row strides
-//                   that are not 16-byte multiples).
+//   kModeFusedTma : rows = raw f32 (I,Q) frames, TMA-staged in shared memory in
+//                   half-K-block chunks (32 samples x 64 links) and converted (remove_cp +
+//                   de-interleave + fp16/bf16) by converter warps straight into the
+//                   128B-swizzled UMMA A stage -- K2 fused away;
+//   kModeFusedLdg : as above but converters LDG the f32 rows (row strides that are not
+//                   16-byte multiples).
 // Warp roles (16 warps, both CTAs unless noted):
-//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader) / arrive forwarder (peer)
-//   2 raw-row TMA producer (FusedTma)                3 spare
-//   4-7 converters (fused)                           8-15 epilogue (2 warps per TMEM lane quarter)
+//   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader CTA only)
+//   2 raw-chunk TMA producer (FusedTma)              3 idle
+//   4-11 converters (fused)                          12-15 epilogue (one per TMEM lane quarter)
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
 
 #ifdef PNCE_DIAG_TRACE
@@ -191,26 +201,28 @@ constexpr int kConvWarp0 = 4;
 constexpr int kConvWarps = 8;
 constexpr int kEpiWarp0 = 12;
 constexpr int kEpiWarps = 4;
-constexpr int kLinksPerTile = kBM / 2;                                        // 64 (re, im) row pairs
-constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 4 (LDG variant)
-constexpr int kRawRowFloats = 2 * kBK + 4;  // one K-block of (I,Q) + 16 B slack for an aligned box start
-constexpr uint32_t kRawStageBytes = kLinksPerTile * kRawRowFloats * 4;         // 64 links: 33 KB
+constexpr int kLinksPerTile = kBM / 2;                                        // 64 links per CTA
+constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 2 (LDG variant)
+constexpr int kRawChunk = kBK / 2;  // samples per raw staging chunk (half a K-block)
 
 struct CorrParams {
-    int64_t total_rows;  // n_frames * n_batches * n_r * 2
-    int32_t m_tiles;     // 256-row tiles (one per CTA pair)
-    int32_t n_groups;    // lag-row groups
-    int32_t g_cols;      // accumulator columns per group (= sum of the MMAs' N)
-    int32_t n_mma;       // MMAs per k-step (1 or 2), each N = nm
+    int64_t total_links;  // n_frames * n_batches * n_r
+    int32_t m_tiles;      // 128-link tiles (one per CTA pair)
+    int32_t n_groups;     // lag-row groups
+    int32_t g_cols;       // accumulator columns per group (= sum of the MMAs' N)
+    int32_t n_mma;        // MMAs per k-step (1 or 2), each N = nm
     int32_t nm;
-    int32_t acc_stages;  // TMEM accumulator buffers (2 if 2*g_cols <= 512)
+    int32_t acc_stages;   // TMEM accumulator buffers (2 if 2*g_cols <= 512)
     int32_t k_blocks;
     int32_t stages;
-    int32_t raw_stages;  // FusedTma: f32 staging ring depth
-    int32_t circ_repl;   // circulant replicas
-    int32_t circ_rows;   // rows per replica
+    int32_t raw_stages;      // FusedTma: f32 staging ring depth (half-K-block chunks)
+    int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
+    uint32_t raw_stage_bytes;
+    int32_t desync_ns;    // start delay of odd clusters (staggers the epilogue drains)
+    int32_t circ_repl;    // circulant replicas
+    int32_t circ_rows;    // rows per replica
     uint32_t stage_bytes;
-    uint32_t tx_bytes;   // transaction bytes per stage for BOTH CTAs of the pair
+    uint32_t tx_bytes;    // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
@@ -233,8 +245,7 @@ __device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, in
     const int chunk = task & 7;
     const int64_t q = link0 + link_local;
     const int k0 = kb * kBK + chunk * 8;
-    const int64_t total_links = p.total_rows >> 1;
-    const bool ok = q < total_links;
+    const bool ok = q < p.total_links;
     const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -261,7 +272,6 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row)
 __device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask& t, int bf16) {
     const int link_local = task >> 3;
     const int chunk = task & 7;
-    const int row_re = 2 * link_local, row_im = row_re + 1;
     uint4 vr, vi;
     vr.x = pack2(t.re[0], t.re[1], bf16);
     vr.y = pack2(t.re[2], t.re[3], bf16);
@@ -271,71 +281,201 @@ __device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask
     vi.y = pack2(t.im[2], t.im[3], bf16);
     vi.z = pack2(t.im[4], t.im[5], bf16);
     vi.w = pack2(t.im[6], t.im[7], bf16);
-    st_shared_v4(swz(sa, row_re, chunk * 16), vr);
-    st_shared_v4(swz(sa, row_im, chunk * 16), vi);
+    st_shared_v4(swz(sa, (int)a_row(link_local, 0), chunk * 16), vr);
+    st_shared_v4(swz(sa, (int)a_row(link_local, 1), chunk * 16), vi);
 }
 
-// Epilogue for one 16-column slice held as raw TMEM words v[0..16) of this thread's row.
-__device__ __forceinline__ void epi_slice(const CorrParams& p, const uint32_t* v, bool odd, bool row_ok,
-                                          int n_first, int n_valid, int64_t out_base, float& s_abs,
-                                          float& s_sq, float& s_bad) {
-    // Re/Im pairing: the even lane keeps columns 0..7, the odd lane columns 8..15.
-    float x[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float send = __uint_as_float(odd ? v[i] : v[8 + i]);
-        x[i] = __shfl_xor_sync(0xffffffffu, send, 1);
+// Output window of one link (f, b, r) for the epilogue.
+struct EpiLink {
+    int64_t out;      // complex index of lag 0 of the link's run in taps[f, r, t, l]; -1 = padding link
+    int64_t f;        // frame-set
+    int n_valid;      // valid lags in the run (n_tx * L)
+    bool vec;         // taps + 2*out is 16-byte aligned (pairs of lags as one 16-byte store)
+    bool tvec;        // same for truth
+};
+
+__device__ __forceinline__ EpiLink make_link(const CorrParams& p, int64_t link) {
+    EpiLink e;
+    if (link >= p.total_links) {
+        e.out = -1;
+        e.f = -1;
+        e.n_valid = 0;
+        e.vec = e.tvec = false;
+        return e;
     }
-    if (!row_ok) return;
-    float o[16];
+    const int r = (int)(link % p.n_r);
+    const int64_t fb = link / p.n_r;
+    const int b = (int)(fb % p.n_batches);
+    e.f = fb / p.n_batches;
+    const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
+    e.n_valid = n_tx * p.l;
+    e.out = ((e.f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
+    e.vec = (reinterpret_cast<uintptr_t>(p.taps + 2 * e.out) & 15) == 0;
+    e.tvec = p.truth != nullptr && (reinterpret_cast<uintptr_t>(p.truth + 2 * e.out) & 15) == 0;
+    return e;
+}
+
+__device__ __forceinline__ void err_acc(float re, float im, float hr, float hi, float& s_abs, float& s_sq) {
+    const float dx = re - hr, dy = im - hi;
+    const float sq = dx * dx + dy * dy;
+    s_sq += sq;
+    s_abs += sqrtf(sq);
+}
+
+// K4 for R repetitions of a 16x256b TMEM load: repetition i holds, for this thread's link,
+// Re (v[4i], v[4i+1]) and Im (v[4i+2], v[4i+3]) of lags n + 8i and n + 8i + 1.
+template <int R>
+__device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v, const EpiLink& e, int n,
+                                         float& s_abs, float& s_sq, float& nf) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        o[2 * i] = (odd ? x[i] : __uint_as_float(v[i])) * p.inv_m;
-        o[2 * i + 1] = (odd ? __uint_as_float(v[8 + i]) : x[i]) * p.inv_m;
-    }
-    if (p.stats != nullptr) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (n_first + i < n_valid && !(isfinite(o[2 * i]) && isfinite(o[2 * i + 1]))) s_bad += 1.f;
-    }
-    const int64_t g = out_base + n_first;  // complex index of the first of 8 outputs
+    for (int i = 0; i < R; ++i) {
+        const int lag = n + 8 * i;
+        const float re0 = __uint_as_float(v[4 * i + 0]) * p.inv_m;
+        const float re1 = __uint_as_float(v[4 * i + 1]) * p.inv_m;
+        const float im0 = __uint_as_float(v[4 * i + 2]) * p.inv_m;
+        const float im1 = __uint_as_float(v[4 * i + 3]) * p.inv_m;
+        if (e.out < 0 || lag >= e.n_valid) continue;
+        if (p.stats != nullptr) {
+            // sticky non-finite detector (inf * 0 = NaN); exact count only when it fires
+            nf = fmaf(re0, 0.f, nf);
+            nf = fmaf(im0, 0.f, nf);
+        }
 #ifdef PNCE_DIAG_NO_STORE
-    if (o[0] == 12345.678f) p.taps[g] = o[1];  // keep the work, drop the stores
-    return;
+        if (re0 == 12345.678f) p.taps[0] = re1 + im0 + im1;  // keep the work, drop the stores
+        continue;
 #endif
-    if (n_first + 8 <= n_valid && (g & 3) == 0) {
-        float* dst = p.taps + 2 * g;
-        st_global_v8(dst, *reinterpret_cast<const float(*)[8]>(&o[0]));
-        st_global_v8(dst + 8, *reinterpret_cast<const float(*)[8]>(&o[8]));
-        if (p.truth != nullptr) {
-            float h[16];
-            ld_global_nc_v8(p.truth + 2 * g, *reinterpret_cast<float(*)[8]>(&h[0]));
-            ld_global_nc_v8(p.truth + 2 * g + 8, *reinterpret_cast<float(*)[8]>(&h[8]));
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float dx = o[2 * i] - h[2 * i], dy = o[2 * i + 1] - h[2 * i + 1];
-                const float sq = dx * dx + dy * dy;
-                s_sq += sq;
-                s_abs += sqrtf(sq);
+        float* dst = p.taps + 2 * (e.out + lag);
+        const float* tr = p.truth + 2 * (e.out + lag);
+        if (lag + 1 < e.n_valid) {
+            if (p.stats != nullptr) {
+                nf = fmaf(re1, 0.f, nf);
+                nf = fmaf(im1, 0.f, nf);
             }
-        }
-    } else {
-        float2* taps = reinterpret_cast<float2*>(p.taps);
-        const float2* truth = reinterpret_cast<const float2*>(p.truth);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (n_first + i < n_valid) {
-                taps[g + i] = make_float2(o[2 * i], o[2 * i + 1]);
-                if (truth != nullptr) {
-                    const float2 h = __ldg(truth + g + i);
-                    const float dx = o[2 * i] - h.x, dy = o[2 * i + 1] - h.y;
-                    const float sq = dx * dx + dy * dy;
-                    s_sq += sq;
-                    s_abs += sqrtf(sq);
+            if (e.vec) {
+                st_global_v4(dst, re0, im0, re1, im1);
+            } else {
+                *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+                *reinterpret_cast<float2*>(dst + 2) = make_float2(re1, im1);
+            }
+            if (p.truth != nullptr) {
+                float4 h;
+                if (e.tvec) {
+                    h = ld_global_nc_v4(tr);
+                } else {
+                    const float2 a = __ldg(reinterpret_cast<const float2*>(tr));
+                    const float2 b = __ldg(reinterpret_cast<const float2*>(tr) + 1);
+                    h = make_float4(a.x, a.y, b.x, b.y);
                 }
+                err_acc(re0, im0, h.x, h.y, s_abs, s_sq);
+                err_acc(re1, im1, h.z, h.w, s_abs, s_sq);
+            }
+        } else {
+            *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+            if (p.truth != nullptr) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(tr));
+                err_acc(re0, im0, a.x, a.y, s_abs, s_sq);
             }
         }
     }
+}
+
+// Drain one 16-lane block (8 links) of the accumulator: TMEM -> x 1/M -> taps (+ scoring).
+// 64-column chunks double-buffered (the next chunk's TMEM load is in flight while the
+// current one is scaled and stored), then 16-column remainder pieces.
+__device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
+                                          float& s_abs, float& s_sq, float& nf) {
+    const int cols = p.g_cols;
+    int c = 0;
+    uint32_t va[32], vb[32];
+    if (cols >= 64) {
+        tmem_ld_16x256b_x8(taddr, va);
+        tmem_wait_ld();
+        while (true) {
+            const bool more = c + 128 <= cols;
+            if (more) tmem_ld_16x256b_x8(taddr + c + 64, vb);
+            epi_reps<8>(p, va, e, n0 + c, s_abs, s_sq, nf);
+            c += 64;
+            if (!more) break;
+            tmem_wait_ld();
+            const bool more2 = c + 128 <= cols;
+            if (more2) tmem_ld_16x256b_x8(taddr + c + 64, va);
+            epi_reps<8>(p, vb, e, n0 + c, s_abs, s_sq, nf);
+            c += 64;
+            if (!more2) break;
+            tmem_wait_ld();
+        }
+    }
+    for (; c < cols; c += 16) {
+        uint32_t v[8];
+        tmem_ld_16x256b_x2(taddr + c, v);
+        tmem_wait_ld();
+        epi_reps<2>(p, v, e, n0 + c, s_abs, s_sq, nf);
+    }
+}
+
+// Fast drain of one 16-lane block when every lag this thread owns is valid, the run is
+// 16-byte aligned and nothing is scored: no per-lag predicates, one pointer per block,
+// 4 FMUL + one 16-byte store per repetition.
+__device__ __forceinline__ void epi_reps_fast(const uint32_t* v, float* dst, float s, int reps) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (i < reps) {
+#ifdef PNCE_DIAG_NO_STORE
+            const float x = __uint_as_float(v[4 * i]) * s;
+            if (x == 12345.678f) dst[0] = x;
+#else
+            st_global_v4(dst + 16 * i, __uint_as_float(v[4 * i + 0]) * s, __uint_as_float(v[4 * i + 2]) * s,
+                         __uint_as_float(v[4 * i + 1]) * s, __uint_as_float(v[4 * i + 3]) * s);
+#endif
+        }
+    }
+}
+
+__device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst) {
+    const int cols = p.g_cols;
+    const float s = p.inv_m;
+    int c = 0;
+    uint32_t va[32], vb[32];
+    if (cols >= 64) {
+        tmem_ld_16x256b_x8(taddr, va);
+        tmem_wait_ld();
+        while (true) {
+            const bool more = c + 128 <= cols;
+            if (more) tmem_ld_16x256b_x8(taddr + c + 64, vb);
+            epi_reps_fast(va, dst + 2 * c, s, 8);
+            c += 64;
+            if (!more) break;
+            tmem_wait_ld();
+            const bool more2 = c + 128 <= cols;
+            if (more2) tmem_ld_16x256b_x8(taddr + c + 64, va);
+            epi_reps_fast(vb, dst + 2 * c, s, 8);
+            c += 64;
+            if (!more2) break;
+            tmem_wait_ld();
+        }
+    }
+    for (; c < cols; c += 16) {
+        uint32_t v[8];
+        tmem_ld_16x256b_x2(taddr + c, v);
+        tmem_wait_ld();
+        epi_reps_fast(v, dst + 2 * c, s, 2);
+    }
+}
+
+// Exact non-finite count of the taps this thread wrote for one link (rare path: only
+// when the sticky detector fired).  Reads back this thread's own stores.
+__device__ __noinline__ float recount_nonfinite(const CorrParams& p, const EpiLink& e, int n0) {
+    float bad = 0.f;
+    for (int c = 0; c < p.g_cols; c += 8)
+        for (int t = 0; t < 2; ++t) {
+            const int lag = n0 + c + t;
+            if (lag < e.n_valid) {
+                const volatile float* v = p.taps + 2 * (e.out + lag);
+                const float x = v[0], y = v[1];
+                if (!(isfinite(x) && isfinite(y))) bad += 1.f;
+            }
+        }
+    return bad;
 }
 
 template <int MODE>
@@ -400,20 +540,27 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const uint32_t a_bytes = kBM * kBK * 2;
     const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
 
+    if (p.desync_ns > 0 && (cid & 1)) {
+        // phase-shift odd clusters so that their store-heavy drains overlap the even
+        // clusters' load-heavy main loops (tiles are equal-length, so the shift persists)
+        uint64_t t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (t - t0 < (uint64_t)p.desync_ns);
+    }
+
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
             const uint64_t pol_in = policy_evict_first();
             const uint64_t pol_circ = policy_evict_last();
             const int circ_row0 = (cid % p.circ_repl) * p.circ_rows;
+            int kb = 0, tile = cid, stage = 0;
+            int mt = tile / p.n_groups, g = tile - mt * p.n_groups;
+            uint32_t phase = 0;
             for (int j = 0; j < jobs; ++j) {
-                const int ti = j / p.k_blocks;
-                const int kb = j - ti * p.k_blocks;
-                const int tile = cid + ti * n_clusters;
-                const int mt = tile / p.n_groups;
-                const int g = tile - mt * p.n_groups;
-                const int stage = j % S;
-                mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+                mbar_wait(&empty[stage], phase ^ 1u);
                 TRACE(0, j);
                 uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
                 uint8_t* sb = sa + a_bytes;
@@ -424,13 +571,20 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
                                      circ_row0 + g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
+                if (++stage == S) { stage = 0; phase ^= 1u; }
+                if (++kb == p.k_blocks) {
+                    kb = 0;
+                    tile += n_clusters;
+                    mt = tile / p.n_groups;
+                    g = tile - mt * p.n_groups;
+                }
             }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
-            int acc = 0;
-            uint32_t acc_phase = 0;
+            int acc = 0, stage = 0;
+            uint32_t acc_phase = 0, phase = 0;
             for (int ti = 0; ti < my_tiles; ++ti) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 TRACE(1, ti);
@@ -438,8 +592,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const int j = ti * p.k_blocks + kb;
-                    const int stage = j % S;
-                    const uint32_t phase = (uint32_t)(j / S) & 1u;
 #ifndef PNCE_DIAG_NO_FULLWAIT
                     mbar_wait(&full[stage], phase);
 #else
@@ -459,6 +611,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     }
                     umma_commit_pair(&empty[stage]);
                     TRACE(3, j);
+                    (void)j;
+                    if (++stage == S) { stage = 0; phase ^= 1u; }
                 }
                 umma_commit_pair(&tfull[acc]);
                 if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
@@ -466,79 +620,98 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         }
     } else if (warp == 2) {
         if (RAW && lane == 0) {
-            // ===== raw-row producer: TMA the f32 (I,Q) rows of this CTA's 64 links for one
-            // K-block (64 links x 64 samples x 8 B = 32 KB) into the staging ring.
+            // ===== raw-chunk producer: TMA the f32 (I,Q) rows of this CTA's 64 links for half a
+            // K-block (64 links x 32 samples x 8 B = 16 KB, +16 B per row when C is odd) into the
+            // staging ring.  Finer chunks = more loads in flight for the same shared memory.
             const uint64_t pol = policy_evict_first();
+            int kb = 0, tile = cid, rs = 0;
+            int mt = tile / p.n_groups;
+            uint32_t rphase = 0;
             for (int j = 0; j < jobs; ++j) {
-                const int ti = j / p.k_blocks;
-                const int kb = j - ti * p.k_blocks;
-                const int mt = (cid + ti * n_clusters) / p.n_groups;
-                const int rs = j % p.raw_stages;
-                mbar_wait(&raw_empty[rs], ((uint32_t)(j / p.raw_stages) & 1u) ^ 1u);
-                TRACE(6, j);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait(&raw_empty[rs], rphase ^ 1u);
+                    if (h == 0) TRACE(6, j);
 #ifdef PNCE_DIAG_NO_RAW
-                mbar_arrive(&raw_full[rs]);
-                (void)pol; (void)mt; (void)kb;
+                    mbar_arrive(&raw_full[rs]);
+                    (void)pol; (void)mt; (void)kb;
 #else
-                mbar_arrive_expect_tx(&raw_full[rs], kRawStageBytes);
-                // box start rounded down to a 16-byte boundary; converters skip the slack
-                tma_load_2d(raw_base + (size_t)rs * kRawStageBytes, &tm_in, &raw_full[rs],
-                            (2 * (p.c + kb * kBK)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile, pol);
+                    mbar_arrive_expect_tx(&raw_full[rs], p.raw_stage_bytes);
+                    // box start rounded down to a 16-byte boundary; converters skip the slack
+                    tma_load_2d(raw_base + (size_t)rs * p.raw_stage_bytes, &tm_in, &raw_full[rs],
+                                (2 * (p.c + kb * kBK + h * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile,
+                                pol);
 #endif
+                    if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
+                }
+                if (++kb == p.k_blocks) {
+                    kb = 0;
+                    tile += n_clusters;
+                    mt = tile / p.n_groups;
+                }
             }
         }
     } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
         if (FUSED) {
             const int cw = warp - kConvWarp0;
+            int ti = 0, kb = 0, stage = 0, rs = 0;
+            uint32_t phase = 0, rphase = 0;
             for (int j = 0; j < jobs; ++j) {
-                const int ti = j / p.k_blocks;
-                const int kb = j - ti * p.k_blocks;
-                const int stage = j % S;
                 const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
                 if (RAW) {
-                    // staged f32 rows -> A stage.  Warp w converts links w, w+4, ...; lane l
-                    // handles samples 2l, 2l+1 (one conflict-free LDS.128 of the 512 B row,
-                    // two STS.32 into the Re / Im rows).
-                    const int rs = j % p.raw_stages;
-                    mbar_wait(&raw_full[rs], (uint32_t)(j / p.raw_stages) & 1u);
-                    if (cw == 0 && lane == 0) TRACE(7, j);
-                    mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+                    // staged f32 chunks -> A stage.  Per chunk a warp converts 8 links: lanes
+                    // 0-15 link a, lanes 16-31 link a+4 (so the two Re rows fall in different
+                    // swizzle halves: conflict-free STS); lane l handles samples 2(l%16), +1
+                    // (one LDS.128 of the link's 256 B row, two STS.32 into its Re / Im rows).
+                    mbar_wait(&empty[stage], phase ^ 1u);
                     if (cw == 0 && lane == 0) TRACE(8, j);
-                    const int slack = (2 * (p.c + kb * kBK)) & 3;  // 0 or 2 floats
-                    const uint32_t raw = smem_u32(raw_base + (size_t)rs * kRawStageBytes) + slack * 4 + lane * 16;
-                    const int k = kb * kBK + 2 * lane;
-                    const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(&raw_full[rs], rphase);
+                        if (h == 0 && cw == 0 && lane == 0) TRACE(7, j);
+                        const int slack = (2 * (p.c + kb * kBK + h * kRawChunk)) & 3;  // 0 or 2 floats
+                        const uint32_t raw =
+                            smem_u32(raw_base + (size_t)rs * p.raw_stage_bytes) + slack * 4 + (lane & 15) * 16;
+                        const int k = kb * kBK + h * kRawChunk + 2 * (lane & 15);
+                        const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
+                        const int col_byte = h * 64 + (lane & 15) * 4;
 #ifndef PNCE_DIAG_NO_CONV
-#pragma unroll 4
-                    for (int i = 0; i < kLinksPerTile / kConvWarps; ++i) {
-                        const int link_local = cw + kConvWarps * i;
-                        float4 v;
-                        if (slack == 0) {
-                            v = ld_shared_v4f(raw + link_local * (kRawRowFloats * 4));
-                        } else {
-                            const float2 a = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4));
-                            const float2 b = ld_shared_v2f(raw + link_local * (kRawRowFloats * 4) + 8);
-                            v = make_float4(a.x, a.y, b.x, b.y);
+#pragma unroll
+                        for (int it = 0; it < kLinksPerTile / (2 * kConvWarps); ++it) {
+                            const int idx = cw + kConvWarps * it;  // 0..31
+                            const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
+                            const uint32_t src = raw + link * (p.raw_row_floats * 4);
+                            float4 v;
+                            if (slack == 0) {
+                                v = ld_shared_v4f(src);
+                            } else {
+                                const float2 a = ld_shared_v2f(src);
+                                const float2 b = ld_shared_v2f(src + 8);
+                                v = make_float4(a.x, a.y, b.x, b.y);
+                            }
+                            if (!ok0) { v.x = 0.f; v.y = 0.f; }
+                            if (!ok1) { v.z = 0.f; v.w = 0.f; }
+                            st_shared_u32(swz(sa, (int)a_row(link, 0), col_byte), pack2(v.x, v.z, p.bf16));
+                            st_shared_u32(swz(sa, (int)a_row(link, 1), col_byte), pack2(v.y, v.w, p.bf16));
                         }
-                        if (!ok0) { v.x = 0.f; v.y = 0.f; }
-                        if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                        st_shared_u32(swz(sa, 2 * link_local, lane * 4), pack2(v.x, v.z, p.bf16));
-                        st_shared_u32(swz(sa, 2 * link_local + 1, lane * 4), pack2(v.y, v.w, p.bf16));
-                    }
 #else
-                    (void)raw; (void)ok0; (void)ok1;
+                        (void)raw; (void)ok0; (void)ok1; (void)col_byte;
 #endif
+                        // the chunk's values are consumed (the STS above depend on them)
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&raw_empty[rs]);
+                        if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
+                    }
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
                         // proxy fence above completed this warp's STS; plain (CTA-scope
                         // release) arrive on the leader's barrier, no GPU-scope membar
                         mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
-                        mbar_arrive(&raw_empty[rs]);
                         if (cw == 0) TRACE(9, j);
                     }
                 } else {
-                    // LDG fallback: 4 tasks (link, 8-sample chunk) per thread
+                    // LDG variant: 2 tasks (link, 8-sample chunk) per thread
                     const int mt = (cid + ti * n_clusters) / p.n_groups;
                     const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
                     const int ct = cw * 32 + lane;
@@ -546,23 +719,23 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #pragma unroll
                     for (int i = 0; i < kTasksPerThread; ++i)
                         conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
-                    mbar_wait(&empty[stage], ((uint32_t)(j / S) & 1u) ^ 1u);
+                    mbar_wait(&empty[stage], phase ^ 1u);
 #pragma unroll
                     for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                 }
+                if (++stage == S) { stage = 0; phase ^= 1u; }
+                if (++kb == p.k_blocks) { kb = 0; ++ti; }
             }
         }
     } else if (warp >= kEpiWarp0) {
-        // ===== epilogue (both CTAs): TMEM lane quarter = warp % 4, column slice = (warp-first)/4
-        constexpr int kSlices = kEpiWarps / 4;
+        // ===== epilogue (both CTAs): warp q = warp % 4 owns TMEM lanes 32q..32q+31 = two
+        // 16-row blocks = links 16q..16q+15 of this CTA's 64; thread t handles link
+        // 8*block + t/4 of its quarter and lags 2(t%4), 2(t%4)+1 of every 8-lag repetition.
         const int quarter = warp & 3;
-        const int half = (warp - kEpiWarp0) >> 2;
-        const int cph = ((p.g_cols + kSlices - 1) / kSlices + 15) / 16 * 16;
-        const int c_begin = min(p.g_cols, half * cph);
-        const int c_end = min(p.g_cols, c_begin + cph);
+        const int colp = 2 * (lane & 3);
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -570,55 +743,43 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int tile = cid + ti * n_clusters;
             const int mt = tile / p.n_groups;
             const int g = tile - mt * p.n_groups;
+            const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
+            const EpiLink e0 = make_link(p, link0);
+            const EpiLink e1 = make_link(p, link0 + 8);
+            const int n0 = g * p.g_cols + colp;
+            if (p.truth != nullptr && (lane & 3) == 0) {
+                // pull this tile's truth windows into L2 while the MMAs run
+                for (int bb = 0; bb < 2; ++bb) {
+                    const EpiLink& e = bb ? e1 : e0;
+                    const int lag0 = g * p.g_cols;
+                    const int n = min(p.g_cols, e.n_valid - lag0);
+                    if (e.out >= 0 && n > 0) {
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.truth + 2 * (e.out + lag0)) & ~uintptr_t(15);
+                        const uintptr_t a1 =
+                            (reinterpret_cast<uintptr_t>(p.truth + 2 * (e.out + lag0 + n)) + 15) & ~uintptr_t(15);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                                     : "memory");
+                    }
+                }
+            }
             mbar_wait(&tfull[acc], acc_phase);
             if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
             tc_fence_after();
 
-            const int64_t row = (int64_t)mt * 2 * kBM + (int64_t)rank * kBM + quarter * 32 + lane;
-            const bool row_ok = row < p.total_rows;
-            const bool odd = (lane & 1) != 0;
-            const int64_t link = row >> 1;
-            const int r = (int)(link % p.n_r);
-            const int64_t fb = link / p.n_r;
-            const int b = (int)(fb % p.n_batches);
-            const int64_t f = fb / p.n_batches;
-            const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
-            const int n_valid = n_tx * p.l;
-            const int64_t out_base = ((f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
-            float s_abs = 0.f, s_sq = 0.f, s_bad = 0.f;
-
-            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * p.g_cols);
-            const int n_tile0 = g * p.g_cols;
-            // 32-column chunks (two 16-column slices each); the next chunk's TMEM load is
-            // in flight while the current one is paired, scaled and stored.
-            uint32_t va[32], vb[32];
-            int c0 = c_begin;
-            if (c0 + 32 <= c_end) {
-                tmem_ld32_nowait(t_row + c0, va);
-                tmem_wait_ld();
-                while (true) {
-                    const bool more = c0 + 64 <= c_end;
-                    if (more) tmem_ld32_nowait(t_row + c0 + 32, vb);
-                    epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, va + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
-                              s_sq, s_bad);
-                    c0 += 32;
-                    if (!more) break;
-                    tmem_wait_ld();
-                    const bool more2 = c0 + 64 <= c_end;
-                    if (more2) tmem_ld32_nowait(t_row + c0 + 32, va);
-                    epi_slice(p, vb, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
-                    epi_slice(p, vb + 16, odd, row_ok, n_tile0 + c0 + 16 + (odd ? 8 : 0), n_valid, out_base, s_abs,
-                              s_sq, s_bad);
-                    c0 += 32;
-                    if (!more2) break;
-                    tmem_wait_ld();
-                }
-            }
-            if (c0 < c_end) {  // 16-column remainder
-                tmem_ld16_nowait(t_row + c0, *reinterpret_cast<uint32_t(*)[16]>(va));
-                tmem_wait_ld();
-                epi_slice(p, va, odd, row_ok, n_tile0 + c0 + (odd ? 8 : 0), n_valid, out_base, s_abs, s_sq, s_bad);
+            float s_abs[2] = {0.f, 0.f}, s_sq[2] = {0.f, 0.f}, nf[2] = {0.f, 0.f};
+            const uint32_t t_acc = tmem_base + (uint32_t)(acc * p.g_cols);
+            const bool plain = p.stats == nullptr;  // no scoring: fast path where the window allows
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb) {
+                const EpiLink& e = bb ? e1 : e0;
+                const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16);
+                // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
+                const bool fast = __all_sync(0xffffffffu, plain && e.out >= 0 && e.vec &&
+                                                              g * p.g_cols + p.g_cols <= e.n_valid);
+                if (fast)
+                    epi_block_fast(p, taddr, p.taps + 2 * (e.out + n0));
+                else
+                    epi_block(p, taddr, e, n0, s_abs[bb], s_sq[bb], nf[bb]);
             }
             // this warp's share of the accumulator is drained -> tell the leader's MMA warp
             tc_fence_before();
@@ -629,31 +790,38 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
 
             if (p.stats != nullptr) {
-                // per-frame reduction: warp-uniform frame -> one atomic per warp.
-                // Rows of a warp are contiguous, so lane 0 holds the first valid row.
-                const bool lead_ok = __shfl_sync(0xffffffffu, row_ok, 0);
-                const int64_t f0 = __shfl_sync(0xffffffffu, f, 0);
-                const bool uniform = __all_sync(0xffffffffu, (f == f0) || !row_ok);
-                if (uniform) {
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
-                        s_sq += __shfl_xor_sync(0xffffffffu, s_sq, o);
-                        s_bad += __shfl_xor_sync(0xffffffffu, s_bad, o);
-                    }
-                    if (lane == 0 && lead_ok) {
-                        if (p.truth != nullptr) {
-                            atomicAdd(&p.stats[f0 * 4 + 0], (double)s_abs);
-                            atomicAdd(&p.stats[f0 * 4 + 1], (double)s_sq);
+                for (int bb = 0; bb < 2; ++bb) {
+                    const EpiLink& e = bb ? e1 : e0;
+                    float bad = 0.f;
+                    if (e.out >= 0 && nf[bb] != 0.f) bad = recount_nonfinite(p, e, n0);
+                    float sa = s_abs[bb], sq = s_sq[bb];
+                    // per-frame reduction: warp-uniform frame -> one atomic per warp.  Links
+                    // ascend with the lane, so lane 0 holds the block's first (valid) link.
+                    const bool lead_ok = __shfl_sync(0xffffffffu, e.out >= 0, 0);
+                    const int64_t f0 = __shfl_sync(0xffffffffu, e.f, 0);
+                    const bool uniform = __all_sync(0xffffffffu, e.f == f0 || e.out < 0);
+                    if (uniform) {
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+                            sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                            bad += __shfl_xor_sync(0xffffffffu, bad, o);
                         }
-                        if (s_bad != 0.f) atomicAdd(&p.stats[f0 * 4 + 2], (double)s_bad);
+                        if (lane == 0 && lead_ok) {
+                            if (p.truth != nullptr) {
+                                atomicAdd(&p.stats[f0 * 4 + 0], (double)sa);
+                                atomicAdd(&p.stats[f0 * 4 + 1], (double)sq);
+                            }
+                            if (bad != 0.f) atomicAdd(&p.stats[f0 * 4 + 2], (double)bad);
+                        }
+                    } else if (e.out >= 0) {
+                        if (p.truth != nullptr) {
+                            atomicAdd(&p.stats[e.f * 4 + 0], (double)sa);
+                            atomicAdd(&p.stats[e.f * 4 + 1], (double)sq);
+                        }
+                        if (bad != 0.f) atomicAdd(&p.stats[e.f * 4 + 2], (double)bad);
                     }
-                } else if (row_ok) {
-                    if (p.truth != nullptr) {
-                        atomicAdd(&p.stats[f * 4 + 0], (double)s_abs);
-                        atomicAdd(&p.stats[f * 4 + 1], (double)s_sq);
-                    }
-                    if (s_bad != 0.f) atomicAdd(&p.stats[f * 4 + 2], (double)s_bad);
                 }
             }
         }
@@ -700,15 +868,16 @@ pnce_status_t make_tmap(CUtensorMap* map, const void* base, uint64_t cols, uint6
     return PNCE_OK;
 }
 
-// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][132 floats]
-// (one K-block of 64 (I,Q) samples for 64 links + 16 B slack so the box start can be
-// rounded down to a 16-byte boundary), no swizzle.
-pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows) {
+// Received f32 rows as a 2-D tensor [links][2*samples] floats, box [64 links][box_floats]
+// (half a K-block = 32 (I,Q) samples for 64 links, + 16 B slack when C is odd so the box
+// start can be rounded down to a 16-byte boundary), no swizzle.
+pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_floats, uint64_t rows,
+                            uint32_t box_floats) {
     auto enc = get_encode();
     if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {row_floats, rows};
     cuuint64_t strides[1] = {row_floats * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kRawRowFloats, (cuuint32_t)kLinksPerTile};
+    cuuint32_t box[2] = {(cuuint32_t)box_floats, (cuuint32_t)kLinksPerTile};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -742,7 +911,7 @@ struct pnce_plan {
                      // the whole grid does not hammer the same L2 lines in lock-step
     int num_sms;
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
-    Tiling packed;   // packed operand in: groups of <= 256 cols, double-buffered accumulator
+    Tiling packed;   // packed operand in: same grouping (A and B per-SM ingress, not the drain, bound G=256)
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
 };
@@ -850,7 +1019,7 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
     const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
     make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
-    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 256);
+    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
     p->rows_alloc = std::max(p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols);
     p->num_sms = sms;
 
@@ -930,7 +1099,8 @@ pnce_status_t pnce_plan_chips(const pnce_plan_t* p, float* dst, void* stream) {
 
 size_t pnce_workspace_bytes(const pnce_plan_t* p, int64_t n_frames) {
     if (!p || n_frames < 0) return 0;
-    const int64_t rows = n_frames * p->n_batches * (int64_t)p->cfg.n_r * 2;
+    const int64_t links = n_frames * p->n_batches * (int64_t)p->cfg.n_r;
+    const int64_t rows = (links + 7) / 8 * 16;  // a_row order: whole 8-link blocks
     return (size_t)rows * p->k_pad * 2;
 }
 
@@ -945,7 +1115,7 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     const pnce_cfg_t& c = p->cfg;
     const int samples = c.c + c.m + c.l - 1;
     const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
-    const int64_t work = links * (p->k_pad / 8);
+    const int64_t work = (links + 7) / 8 * 8 * (p->k_pad / 8);
     const int64_t want = (work + 255) / 256;
     const int blocks = (int)(want < (int64_t)p->num_sms * 16 ? want : (int64_t)p->num_sms * 16);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -958,6 +1128,8 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     return PNCE_OK;
 }
 
+static bool c_odd(const pnce_plan_t* p) { return (p->cfg.c & 1) != 0; }
+
 // Shared launch setup for both K3 variants.
 static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fused, float* taps, const float* truth,
                                  double* stats, int64_t n_frames, CorrParams& prm) {
@@ -965,12 +1137,14 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
         return fail(PNCE_ERR_DIMENSION, "taps/truth must be 8-byte aligned");
     const pnce_cfg_t& c = p->cfg;
     prm = CorrParams{};
-    prm.total_rows = n_frames * p->n_batches * (int64_t)c.n_r * 2;
-    const int64_t m_tiles = (prm.total_rows + 2 * kBM - 1) / (2 * kBM);
-    if (m_tiles * t.n_groups > INT32_MAX || prm.total_rows > INT32_MAX)
+    prm.total_links = n_frames * p->n_batches * (int64_t)c.n_r;
+    const int64_t m_tiles = (prm.total_links + kBM - 1) / kBM;
+    if (m_tiles * t.n_groups > INT32_MAX || 2 * prm.total_links > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
     prm.circ_repl = p->repl;
+    const char* ds = std::getenv("PNCE_TUNE_DESYNC_NS");
+    prm.desync_ns = ds ? std::max(0, std::atoi(ds)) : 0;
     prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
     prm.g_cols = t.g_cols;
@@ -1017,7 +1191,9 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     pnce_status_t s = fill_params(p, p->packed, false, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     CUtensorMap tm_in;
-    s = make_tmap(&tm_in, packed, p->k_pad, (uint64_t)prm.total_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
+    // packed rows: 2 per link, padded to whole 8-link blocks (a_row order)
+    const uint64_t packed_rows = (uint64_t)((prm.total_links + 7) / 8) * 16;
+    s = make_tmap(&tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) return s;
     const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
     k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, static_cast<cudaStream_t>(stream)>>>(
@@ -1047,20 +1223,26 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     if (fm && std::atoi(fm) == kModeFusedLdg) raw_ok = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (raw_ok) {
-        // f32 rows TMA-staged in shared memory (default): raw ring + A/B ring
-        const char* rs = std::getenv("PNCE_TUNE_RAW_STAGES");
-        prm.raw_stages = rs ? std::max(1, std::atoi(rs)) : 2;
-        const int64_t avail = (int64_t)kSmemLimit - 2048 - (int64_t)prm.raw_stages * kRawStageBytes;
-        int ab = (int)std::min<int64_t>(8, avail / (int64_t)prm.stage_bytes);
+        // f32 rows TMA-staged in shared memory (default): A/B ring of up to 3 stages, the
+        // rest of shared memory as the raw half-K-block ring (its depth hides HBM latency:
+        // ~1.3 us per load vs ~0.4 us of MMA per chunk)
+        prm.raw_row_floats = 2 * kRawChunk + ((c_odd(p)) ? 4 : 0);
+        prm.raw_stage_bytes = (uint32_t)(kLinksPerTile * prm.raw_row_floats * 4);
+        const int64_t budget = (int64_t)kSmemLimit - 2048;
+        int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
         const char* as = std::getenv("PNCE_TUNE_AB_STAGES");
-        if (as) ab = std::min(ab, std::max(1, std::atoi(as)));
-        if (ab < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        if (as) ab = std::min<int>((int)(budget / prm.stage_bytes), std::max(1, std::atoi(as)));
+        int raw = (int)std::min<int64_t>(8, (budget - (int64_t)ab * prm.stage_bytes) / prm.raw_stage_bytes);
+        const char* rs = std::getenv("PNCE_TUNE_RAW_STAGES");
+        if (rs) raw = std::min(raw, std::max(1, std::atoi(rs)));
+        if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
+        prm.raw_stages = raw;
         CUtensorMap tm_raw;
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)(prm.total_rows / 2));
+        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);
         if (s != PNCE_OK) return s;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
-                            (size_t)prm.raw_stages * kRawStageBytes;
+                            (size_t)prm.raw_stages * prm.raw_stage_bytes;
         k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
 #ifdef PNCE_DIAG_TRACE
         if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {

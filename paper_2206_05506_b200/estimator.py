@@ -237,10 +237,12 @@ class Correlator:
         return taps_host
 
     def pack(self, iq: torch.Tensor) -> torch.Tensor:
-        """K2 alone: returns the packed 16-bit operand (rows = F*n_batches*n_r*2, K_pad)."""
+        """K2 alone: returns the packed 16-bit operand (K_pad columns; rows in 16-row blocks of
+        8 links, Re rows then Im rows -- see pnce_workspace_bytes in include/pnce_b200.h)."""
         iq, n_frames = self._check_iq(iq)
         k_pad = -(-self.cfg.m // 64) * 64
-        rows = n_frames * self.cfg.n_batches * self.n_r * 2
+        links = n_frames * self.cfg.n_batches * self.n_r
+        rows = -(-links // 8) * 16
         tdt = torch.float16 if self.dtype == "fp16" else torch.bfloat16
         packed = torch.empty((rows, k_pad), dtype=tdt, device=self.device)
         with torch.cuda.device(self.device):

@@ -78,16 +78,21 @@ def test_device_lfsr_state_and_rejection(dev):
 
 
 # ------------------------------------------------------------------ a4: pack
-@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
-def test_pack_bit_exact(dev, dtype):
-    cfg, ocfg = make_cfg(16, 255, 32, 4)
-    chips, iq, _ = sim_sets(ocfg, 2)
-    corr = P.Correlator(P.default_spec(8), cfg, 16, dtype=dtype, device=dev)
+@pytest.mark.parametrize("dtype,n_r,n_sets", [("fp16", 16, 2), ("bf16", 16, 2), ("fp16", 3, 1)])
+def test_pack_bit_exact(dev, dtype, n_r, n_sets):
+    cfg, ocfg = make_cfg(16, 255, 32, 4, n_r=n_r)
+    chips, iq, _ = sim_sets(ocfg, n_sets)
+    corr = P.Correlator(P.default_spec(8), cfg, n_r, dtype=dtype, device=dev)
     packed = corr.pack(torch.from_numpy(iq).to(dev)).cpu()
     body = iq[..., cfg.c:cfg.c + cfg.m, :]                     # (F, nb, n_r, M, 2)
-    rows = np.moveaxis(body, -1, -2).reshape(-1, cfg.m)        # rows (f, b, r, part)
+    links = np.moveaxis(body, -1, -2).reshape(-1, 2, cfg.m)    # (link, part, M)
+    pad = -len(links) % 8
+    links = np.concatenate([links, np.zeros((pad, 2, cfg.m), links.dtype)])
+    # 16-row blocks of 8 links: the 8 Re rows, then the 8 Im rows
+    rows = links.reshape(-1, 8, 2, cfg.m).transpose(0, 2, 1, 3).reshape(-1, cfg.m)
     tdt = torch.float16 if dtype == "fp16" else torch.bfloat16
-    want = torch.from_numpy(rows).to(tdt)
+    want = torch.from_numpy(np.ascontiguousarray(rows)).to(tdt)
+    assert packed.shape[0] == len(rows)
     assert torch.equal(packed[:, :cfg.m], want)
     assert torch.count_nonzero(packed[:, cfg.m:]) == 0
 
