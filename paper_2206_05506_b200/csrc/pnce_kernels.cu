@@ -195,6 +195,22 @@ __device__ __forceinline__ long long gtimer() {
     do {                 \
     } while (0)
 #endif
+#ifdef PNCE_DIAG_PROF
+// Cycle accounting (clock64, kept in registers, written once per role at the end):
+// per CTA 16 slots, see kProf* below.
+constexpr int kProfSlots = 16;
+__device__ unsigned long long g_prof[1024 * kProfSlots];
+#define PROF_BEGIN(n) uint64_t _pacc[n] = {}; uint64_t _pt = clock64()
+#define PROF_MARK(i) do { const uint64_t _n = clock64(); _pacc[i] += _n - _pt; _pt = _n; } while (0)
+#define PROF_END(base, n) do { for (int _i = 0; _i < (n); ++_i) g_prof[blockIdx.x * kProfSlots + (base) + _i] = _pacc[_i]; } while (0)
+#else
+#define PROF_BEGIN(n) do { } while (0)
+#define PROF_MARK(i) do { } while (0)
+#define PROF_END(base, n) do { } while (0)
+#endif
+// slots: B producer {wait empty, issue} 0-1; MMA {wait tempty, wait full, issue} 2-4;
+// raw producer {wait raw_empty, issue} 5-6; converter {wait empty, wait raw, convert} 7-9;
+// epilogue {wait tfull, drain} 10-11; MMA total 12
 constexpr int kWarps = 16;
 constexpr int kThreadsK3 = kWarps * 32;
 constexpr int kConvWarp0 = 4;
@@ -202,7 +218,6 @@ constexpr int kConvWarps = 8;
 constexpr int kEpiWarp0 = 12;
 constexpr int kEpiWarps = 4;
 constexpr int kLinksPerTile = kBM / 2;                                        // 64 links per CTA
-constexpr int kTasksPerThread = kLinksPerTile * (kBK / 8) / (kConvWarps * 32);  // 2 (LDG variant)
 constexpr int kRawChunk = kBK / 2;  // samples per raw staging chunk (half a K-block)
 
 struct CorrParams {
@@ -219,6 +234,8 @@ struct CorrParams {
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
     int32_t desync_ns;    // start delay of odd clusters (staggers the epilogue drains)
+    int32_t raw_prefetch; // raw chunks prefetched into L2 ahead of their load (0 = off)
+    int32_t raw_map;      // tm_in is the raw f32 map (L2 prefetch possible in LDG mode)
     int32_t circ_repl;    // circulant replicas
     int32_t circ_rows;    // rows per replica
     uint32_t stage_bytes;
@@ -235,26 +252,6 @@ struct CorrParams {
     double* stats;
 };
 
-// One LDG-converter task: 8 consecutive body samples of one link.
-struct ConvTask {
-    float re[8], im[8];
-};
-
-__device__ __forceinline__ void conv_load(const CorrParams& p, int64_t link0, int kb, int task, ConvTask& t) {
-    const int link_local = task >> 3;
-    const int chunk = task & 7;
-    const int64_t q = link0 + link_local;
-    const int k0 = kb * kBK + chunk * 8;
-    const bool ok = q < p.total_links;
-    const float2* s2 = reinterpret_cast<const float2*>(p.iq) + (ok ? q * p.samples + p.c + k0 : 0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const float2 v = (ok && k0 + j < p.m) ? __ldg(s2 + j) : make_float2(0.f, 0.f);
-        t.re[j] = v.x;
-        t.im[j] = v.y;
-    }
-}
-
 __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
     if (bf16) {
         __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -267,22 +264,6 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
 // 128B swizzle of the UMMA K-major A stage: 16-byte chunk c of row r lives at chunk c ^ (r % 8).
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row) {
     return base + row * 128 + ((((byte_in_row >> 4) ^ (row & 7))) << 4) + (byte_in_row & 15);
-}
-
-__device__ __forceinline__ void conv_store(uint32_t sa, int task, const ConvTask& t, int bf16) {
-    const int link_local = task >> 3;
-    const int chunk = task & 7;
-    uint4 vr, vi;
-    vr.x = pack2(t.re[0], t.re[1], bf16);
-    vr.y = pack2(t.re[2], t.re[3], bf16);
-    vr.z = pack2(t.re[4], t.re[5], bf16);
-    vr.w = pack2(t.re[6], t.re[7], bf16);
-    vi.x = pack2(t.im[0], t.im[1], bf16);
-    vi.y = pack2(t.im[2], t.im[3], bf16);
-    vi.z = pack2(t.im[4], t.im[5], bf16);
-    vi.w = pack2(t.im[6], t.im[7], bf16);
-    st_shared_v4(swz(sa, (int)a_row(link_local, 0), chunk * 16), vr);
-    st_shared_v4(swz(sa, (int)a_row(link_local, 1), chunk * 16), vi);
 }
 
 // Output window of one link (f, b, r) for the epilogue.
@@ -478,6 +459,17 @@ __device__ __noinline__ float recount_nonfinite(const CorrParams& p, const EpiLi
     return bad;
 }
 
+// L2 prefetch of raw chunk `jc` (= 2 * job + half) of this cluster's job list.
+__device__ __forceinline__ void prefetch_raw_chunk(const CorrParams& p, const CUtensorMap* tm, int jc, int jobs,
+                                                   int cid, int n_clusters, uint32_t rank) {
+    const int j = jc >> 1;
+    if (j >= jobs) return;
+    const int ti = j / p.k_blocks;
+    const int kb = j - ti * p.k_blocks;
+    const int mt = (cid + ti * n_clusters) / p.n_groups;
+    tma_prefetch_l2_2d(tm, (2 * (p.c + kb * kBK + (jc & 1) * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile);
+}
+
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
@@ -507,7 +499,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         for (int s = 0; s < S; ++s) {
             // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
             // bytes and converter arrives land on the leader's barrier).
-            mbar_init(&full[s], FUSED ? 1 + 2 * kConvWarps : 1);
+            // (LDG mode: only one 4-warp group converts a given stage)
+            mbar_init(&full[s], RAW ? 1 + 2 * kConvWarps : (FUSED ? 1 + kConvWarps : 1));
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -559,8 +552,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             int kb = 0, tile = cid, stage = 0;
             int mt = tile / p.n_groups, g = tile - mt * p.n_groups;
             uint32_t phase = 0;
+            PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1u);
+                PROF_MARK(0);
                 TRACE(0, j);
                 uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
                 uint8_t* sb = sa + a_bytes;
@@ -578,15 +573,22 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     mt = tile / p.n_groups;
                     g = tile - mt * p.n_groups;
                 }
+                PROF_MARK(1);
             }
+            PROF_END(0, 2);
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
             int acc = 0, stage = 0;
             uint32_t acc_phase = 0, phase = 0;
+#ifdef PNCE_DIAG_PROF
+            const uint64_t t_start = clock64();
+#endif
+            PROF_BEGIN(3);
             for (int ti = 0; ti < my_tiles; ++ti) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
+                PROF_MARK(0);
                 TRACE(1, ti);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
@@ -597,6 +599,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #else
                     (void)phase;
 #endif
+                    PROF_MARK(1);
                     TRACE(2, j);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -613,12 +616,30 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     TRACE(3, j);
                     (void)j;
                     if (++stage == S) { stage = 0; phase ^= 1u; }
+                    PROF_MARK(2);
                 }
                 umma_commit_pair(&tfull[acc]);
                 if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
+            PROF_END(2, 3);
+#ifdef PNCE_DIAG_PROF
+            g_prof[blockIdx.x * kProfSlots + 12] = clock64() - t_start;
+#endif
         }
     } else if (warp == 2) {
+        if (!RAW && FUSED && p.raw_map && p.raw_prefetch > 0 && lane == 0) {
+            // ===== LDG mode: keep the raw rows of the next jobs in L2 (paced by the stages)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int jc = 0; jc < p.raw_prefetch && jc < 2 * jobs; ++jc)
+                prefetch_raw_chunk(p, &tm_in, jc, jobs, cid, n_clusters, rank);
+            for (int j = 0; j < jobs; ++j) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                prefetch_raw_chunk(p, &tm_in, 2 * j + p.raw_prefetch, jobs, cid, n_clusters, rank);
+                prefetch_raw_chunk(p, &tm_in, 2 * j + 1 + p.raw_prefetch, jobs, cid, n_clusters, rank);
+                if (++stage == S) { stage = 0; phase ^= 1u; }
+            }
+        }
         if (RAW && lane == 0) {
             // ===== raw-chunk producer: TMA the f32 (I,Q) rows of this CTA's 64 links for half a
             // K-block (64 links x 32 samples x 8 B = 16 KB, +16 B per row when C is odd) into the
@@ -627,15 +648,19 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             int kb = 0, tile = cid, rs = 0;
             int mt = tile / p.n_groups;
             uint32_t rphase = 0;
+            PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     mbar_wait(&raw_empty[rs], rphase ^ 1u);
+                    PROF_MARK(0);
                     if (h == 0) TRACE(6, j);
 #ifdef PNCE_DIAG_NO_RAW
                     mbar_arrive(&raw_full[rs]);
                     (void)pol; (void)mt; (void)kb;
 #else
+                    if (p.raw_prefetch > 0)
+                        prefetch_raw_chunk(p, &tm_in, 2 * j + h + p.raw_prefetch, jobs, cid, n_clusters, rank);
                     mbar_arrive_expect_tx(&raw_full[rs], p.raw_stage_bytes);
                     // box start rounded down to a 16-byte boundary; converters skip the slack
                     tma_load_2d(raw_base + (size_t)rs * p.raw_stage_bytes, &tm_in, &raw_full[rs],
@@ -643,6 +668,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                                 pol);
 #endif
                     if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
+                    PROF_MARK(1);
                 }
                 if (++kb == p.k_blocks) {
                     kb = 0;
@@ -650,24 +676,27 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     mt = tile / p.n_groups;
                 }
             }
+            PROF_END(5, 2);
         }
     } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
-        if (FUSED) {
+        if (RAW) {
             const int cw = warp - kConvWarp0;
-            int ti = 0, kb = 0, stage = 0, rs = 0;
+            int kb = 0, stage = 0, rs = 0;
             uint32_t phase = 0, rphase = 0;
+            PROF_BEGIN(3);
             for (int j = 0; j < jobs; ++j) {
                 const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-                if (RAW) {
                     // staged f32 chunks -> A stage.  Per chunk a warp converts 8 links: lanes
                     // 0-15 link a, lanes 16-31 link a+4 (so the two Re rows fall in different
                     // swizzle halves: conflict-free STS); lane l handles samples 2(l%16), +1
                     // (one LDS.128 of the link's 256 B row, two STS.32 into its Re / Im rows).
                     mbar_wait(&empty[stage], phase ^ 1u);
+                    PROF_MARK(0);
                     if (cw == 0 && lane == 0) TRACE(8, j);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait(&raw_full[rs], rphase);
+                        PROF_MARK(1);
                         if (h == 0 && cw == 0 && lane == 0) TRACE(7, j);
                         const int slack = (2 * (p.c + kb * kBK + h * kRawChunk)) & 3;  // 0 or 2 floats
                         const uint32_t raw =
@@ -701,6 +730,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&raw_empty[rs]);
                         if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
+                        PROF_MARK(2);
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -710,25 +740,75 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                         if (cw == 0) TRACE(9, j);
                     }
-                } else {
-                    // LDG variant: 2 tasks (link, 8-sample chunk) per thread
-                    const int mt = (cid + ti * n_clusters) / p.n_groups;
-                    const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile;
-                    const int ct = cw * 32 + lane;
-                    ConvTask buf[kTasksPerThread];
-#pragma unroll
-                    for (int i = 0; i < kTasksPerThread; ++i)
-                        conv_load(p, link0, kb, i * kConvWarps * 32 + ct, buf[i]);
-                    mbar_wait(&empty[stage], phase ^ 1u);
-#pragma unroll
-                    for (int i = 0; i < kTasksPerThread; ++i) conv_store(sa, i * kConvWarps * 32 + ct, buf[i], p.bf16);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
-                }
+                PROF_MARK(2);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
-                if (++kb == p.k_blocks) { kb = 0; ++ti; }
+                if (++kb == p.k_blocks) kb = 0;
             }
+            if (cw == 0 && lane == 0) PROF_END(7, 3);
+        } else if (FUSED) {
+            // ===== pipelined LDG converters.  Group gsel (warps 4-7 / 8-11) converts the jobs
+            // j = gsel (mod 2); each thread holds one K-block of its 16 links' samples in
+            // registers (64 links x 64 samples per group = 32 KB in flight per group), issued
+            // right AFTER the previous job's proxy fence -- fence.proxy.async waits for the
+            // thread's outstanding loads, so loads must never straddle it.  Loads go through
+            // L1 (LDG), a separate ingress path from the TMA engine that feeds the circulant.
+            const int cw = warp - kConvWarp0;
+            const int gsel = cw >> 2, gw = cw & 3;
+            const bool vec = ((p.samples | p.c) & 1) == 0 && (reinterpret_cast<uintptr_t>(p.iq) & 15) == 0;
+            float4 v[kLinksPerTile / 4];
+            int kb = gsel % p.k_blocks, ti = gsel / p.k_blocks;
+            int stage = gsel % S;
+            uint32_t phase = (uint32_t)(gsel / S) & 1u;
+            auto load_job = [&](int lti, int lkb) {
+                const int mt = (cid + lti * n_clusters) / p.n_groups;
+                const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + gw;
+                const int k = lkb * kBK + 2 * lane;
+                const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
+#pragma unroll
+                for (int q = 0; q < kLinksPerTile / 4; ++q) {
+                    const int64_t link = link0 + 4 * q;
+                    const float* src = p.iq + 2 * (link * p.samples + p.c + k);
+                    if (link < p.total_links && ok1 && vec) {
+                        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                     : "=f"(v[q].x), "=f"(v[q].y), "=f"(v[q].z), "=f"(v[q].w)
+                                     : "l"(src));
+                    } else {
+                        const bool l_ok = link < p.total_links;
+                        const float2 a = (l_ok && ok0) ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0.f, 0.f);
+                        const float2 b = (l_ok && ok1) ? __ldg(reinterpret_cast<const float2*>(src) + 1) : make_float2(0.f, 0.f);
+                        v[q] = make_float4(a.x, a.y, b.x, b.y);
+                    }
+                }
+            };
+            if (gsel < jobs) load_job(ti, kb);
+            PROF_BEGIN(3);
+            for (int j = gsel; j < jobs; j += 2) {
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                mbar_wait(&empty[stage], phase ^ 1u);
+                PROF_MARK(0);
+                if (cw == 0 && lane == 0) TRACE(8, j);
+#pragma unroll
+                for (int q = 0; q < kLinksPerTile / 4; ++q) {
+                    // link 4q + gw of the tile; lane -> samples 2*lane, 2*lane+1 (one 128 B row)
+                    const int link_local = 4 * q + gw;
+                    st_shared_u32(swz(sa, (int)a_row(link_local, 0), lane * 4), pack2(v[q].x, v[q].z, p.bf16));
+                    st_shared_u32(swz(sa, (int)a_row(link_local, 1), lane * 4), pack2(v[q].y, v[q].w, p.bf16));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                    if (cw == 0) TRACE(9, j);
+                }
+                // advance two jobs and prefetch the next one (after the fence)
+                stage += 2;
+                while (stage >= S) { stage -= S; phase ^= 1u; }
+                kb += 2;
+                while (kb >= p.k_blocks) { kb -= p.k_blocks; ++ti; }
+                if (j + 2 < jobs) load_job(ti, kb);
+                PROF_MARK(2);
+            }
+            if (cw == 0 && lane == 0) PROF_END(7, 3);
         }
     } else if (warp >= kEpiWarp0) {
         // ===== epilogue (both CTAs): warp q = warp % 4 owns TMEM lanes 32q..32q+31 = two
@@ -739,6 +819,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t acc_phase = 0;
+        PROF_BEGIN(2);
         for (int ti = 0; ti < my_tiles; ++ti) {
             const int tile = cid + ti * n_clusters;
             const int mt = tile / p.n_groups;
@@ -763,6 +844,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
             }
             mbar_wait(&tfull[acc], acc_phase);
+            PROF_MARK(0);
             if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
             tc_fence_after();
 
@@ -788,6 +870,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
             if (lane == 0 && warp == kEpiWarp0 + kEpiWarps - 1) TRACE(12, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
+            PROF_MARK(1);
 
             if (p.stats != nullptr) {
 #pragma unroll
@@ -825,6 +908,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
             }
         }
+        if (warp == kEpiWarp0 && lane == 0) PROF_END(10, 2);
     }
 
     __syncwarp();
@@ -1145,6 +1229,8 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.circ_repl = p->repl;
     const char* ds = std::getenv("PNCE_TUNE_DESYNC_NS");
     prm.desync_ns = ds ? std::max(0, std::atoi(ds)) : 0;
+    const char* rp = std::getenv("PNCE_TUNE_RAW_PREFETCH");
+    prm.raw_prefetch = rp ? std::max(0, std::atoi(rp)) : 0;  // measured: L2 prefetch of raw rows only adds traffic
     prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
     prm.g_cols = t.g_cols;
@@ -1219,14 +1305,22 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     prm.iq = iq;
     const int samples = prm.samples;
     const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
-    bool raw_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
-    if (fm && std::atoi(fm) == kModeFusedLdg) raw_ok = false;
+    // the raw f32 rows can be described by a tensor map when the row stride is 16-byte aligned
+    const bool map_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
+    bool use_tma = map_ok;
+    if (fm && std::atoi(fm) == kModeFusedLdg) use_tma = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (raw_ok) {
+    prm.raw_row_floats = 2 * kRawChunk + ((c_odd(p)) ? 4 : 0);
+    CUtensorMap tm_raw;
+    if (map_ok) {
+        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);
+        if (s != PNCE_OK) return s;
+        prm.raw_map = 1;
+    }
+    if (use_tma) {
         // f32 rows TMA-staged in shared memory (default): A/B ring of up to 3 stages, the
         // rest of shared memory as the raw half-K-block ring (its depth hides HBM latency:
         // ~1.3 us per load vs ~0.4 us of MMA per chunk)
-        prm.raw_row_floats = 2 * kRawChunk + ((c_odd(p)) ? 4 : 0);
         prm.raw_stage_bytes = (uint32_t)(kLinksPerTile * prm.raw_row_floats * 4);
         const int64_t budget = (int64_t)kSmemLimit - 2048;
         int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
@@ -1238,29 +1332,38 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
         prm.raw_stages = raw;
-        CUtensorMap tm_raw;
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);
-        if (s != PNCE_OK) return s;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
                             (size_t)prm.raw_stages * prm.raw_stage_bytes;
         k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
-#ifdef PNCE_DIAG_TRACE
-        if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
-            static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
-            cudaStreamSynchronize(st);
-            cudaMemcpyFromSymbol(host.data(), g_trace, host.size() * sizeof(long long));
-            if (FILE* fh = std::fopen(tf, "wb")) {
-                std::fwrite(host.data(), sizeof(long long), host.size(), fh);
-                std::fclose(fh);
-            }
-        }
-#endif
     } else {
+        if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        // tm_in is unused by the LDG-fused variant; pass the circulant map in its slot.
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(p->fused.tm_circ,
+        // tm_in (the raw map) only serves the L2 prefetcher in the LDG variant
+        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(map_ok ? tm_raw : p->fused.tm_circ,
                                                                                    p->fused.tm_circ, prm);
     }
+#ifdef PNCE_DIAG_PROF
+    if (const char* pf = std::getenv("PNCE_PROF_FILE")) {
+        static std::vector<unsigned long long> host(1024 * kProfSlots);
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host.data(), g_prof, host.size() * sizeof(unsigned long long));
+        if (FILE* fh = std::fopen(pf, "wb")) {
+            std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fh);
+            std::fclose(fh);
+        }
+    }
+#endif
+#ifdef PNCE_DIAG_TRACE
+    if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
+        static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host.data(), g_trace, host.size() * sizeof(long long));
+        if (FILE* fh = std::fopen(tf, "wb")) {
+            std::fwrite(host.data(), sizeof(long long), host.size(), fh);
+            std::fclose(fh);
+        }
+    }
+#endif
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;

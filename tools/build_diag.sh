@@ -11,3 +11,6 @@ $B -DPNCE_DIAG_TRACE -DPNCE_DIAG_NO_STORE -DPNCE_DIAG_NO_RAW -DPNCE_DIAG_NO_CONV
 wait
 $B -DPNCE_DIAG_NO_STORE -DPNCE_DIAG_NO_RAW -DPNCE_DIAG_NO_CONV -DPNCE_DIAG_NO_FULLWAIT -o tools/bin/libpnce_diag_mma_only.so $SRC
 $B -DPNCE_DIAG_TRACE -DPNCE_DIAG_NO_STORE -DPNCE_DIAG_NO_RAW -DPNCE_DIAG_NO_CONV -DPNCE_DIAG_NO_FULLWAIT -o tools/bin/libpnce_diag_trace_mma.so $SRC
+$B -DPNCE_DIAG_PROF -o tools/bin/libpnce_diag_prof.so $SRC &
+$B -DPNCE_DIAG_PROF -DPNCE_DIAG_NO_STORE -o tools/bin/libpnce_diag_prof_nostore.so $SRC &
+wait
