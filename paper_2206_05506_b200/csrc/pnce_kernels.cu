@@ -170,11 +170,15 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
 //                   128B-swizzled UMMA A stage -- K2 fused away;
 //   kModeFusedLdg : as above but converters LDG the f32 rows (row strides that are not
 //                   16-byte multiples).
+//   kModePackedLdg: packed 16-bit rows LDG'd by the converter warps into the A stage (a
+//                   separate ingress path from the TMA engine, which then only carries the
+//                   circulant), so a 256-column double-buffered accumulator can hide the
+//                   epilogue drain without exceeding the TMA ingress rate.
 // Warp roles (16 warps, both CTAs unless noted):
 //   0 TMA producer (circulant rows; + packed rows)   1 MMA issuer (leader CTA only)
 //   2 raw-chunk TMA producer (FusedTma)              3 idle
 //   4-11 converters (fused)                          12-15 epilogue (one per TMEM lane quarter)
-enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2 };
+enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2, kModePackedLdg = 3 };
 
 #ifdef PNCE_DIAG_TRACE
 // Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
@@ -247,6 +251,9 @@ struct CorrParams {
     int32_t bf16;
     float inv_m;
     const float* iq;
+    const uint16_t* packed;  // kModePackedLdg: packed operand, packed_rows x K_pad
+    int64_t packed_rows;
+    int32_t k_pad;
     float* taps;
     const float* truth;
     double* stats;
@@ -474,8 +481,14 @@ template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
-    constexpr bool FUSED = MODE != kModePacked;
-    constexpr bool RAW = MODE == kModeFusedTma;
+    constexpr bool A_TMA = MODE == kModePacked;     // A via TMA with the circulant
+    constexpr bool RAW = MODE == kModeFusedTma;     // f32 rows TMA-staged, converted
+    constexpr bool FLDG = MODE == kModeFusedLdg;    // f32 rows LDG'd, converted
+    constexpr bool PLDG = MODE == kModePackedLdg;   // packed 16-bit rows LDG'd
+    constexpr bool FUSED = RAW || FLDG;
+    // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
+    // one 2-warp group (PLDG)
+    constexpr int kConvArrivals = RAW ? 2 * kConvWarps : (FLDG ? kConvWarps : (PLDG ? kConvWarps / 2 : 0));
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -500,7 +513,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
             // bytes and converter arrives land on the leader's barrier).
             // (LDG mode: only one 4-warp group converts a given stage)
-            mbar_init(&full[s], RAW ? 1 + 2 * kConvWarps : (FUSED ? 1 + kConvWarps : 1));
+            mbar_init(&full[s], 1 + kConvArrivals);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -516,7 +529,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        if (!FUSED || RAW) tma_prefetch(&tm_in);
+        if (A_TMA || RAW || (FLDG && p.raw_map)) tma_prefetch(&tm_in);
         tma_prefetch(&tm_circ);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
@@ -561,7 +574,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 uint8_t* sb = sa + a_bytes;
                 const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
                 if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-                if (!FUSED)
+                if (A_TMA)
                     tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
@@ -627,7 +640,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #endif
         }
     } else if (warp == 2) {
-        if (!RAW && FUSED && p.raw_map && p.raw_prefetch > 0 && lane == 0) {
+        if (FLDG && p.raw_map && p.raw_prefetch > 0 && lane == 0) {
             // ===== LDG mode: keep the raw rows of the next jobs in L2 (paced by the stages)
             int stage = 0;
             uint32_t phase = 0;
@@ -745,7 +758,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 if (++kb == p.k_blocks) kb = 0;
             }
             if (cw == 0 && lane == 0) PROF_END(7, 3);
-        } else if (FUSED) {
+        } else if (FLDG) {
             // ===== pipelined LDG converters.  Group gsel (warps 4-7 / 8-11) converts the jobs
             // j = gsel (mod 2); each thread holds one K-block of its 16 links' samples in
             // registers (64 links x 64 samples per group = 32 KB in flight per group), issued
@@ -806,6 +819,59 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 kb += 2;
                 while (kb >= p.k_blocks) { kb -= p.k_blocks; ++ti; }
                 if (j + 2 < jobs) load_job(ti, kb);
+                PROF_MARK(2);
+            }
+            if (cw == 0 && lane == 0) PROF_END(7, 3);
+        }
+        if (PLDG) {
+            // ===== packed rows via LDG: 4 groups of 2 warps; group g copies the A tiles of
+            // jobs j = g (mod 4).  Thread t of a group holds 16 of the stage's 128 rows x 8
+            // 16-byte chunks in registers (64 KB in flight per CTA), loaded after the
+            // previous job's proxy fence, and stores them into the 128B-swizzled stage.
+            const int cw = warp - kConvWarp0;
+            constexpr int kGroups = 4;
+            const int gsel = cw >> 1;
+            const int tid = (cw & 1) * 32 + lane;  // 0..63
+            uint4 v[16];
+            int kb = gsel % p.k_blocks, ti = gsel / p.k_blocks;
+            int stage = gsel % S;
+            uint32_t phase = (uint32_t)(gsel / S) & 1u;
+            auto load_job = [&](int lti, int lkb) {
+                const int mt = (cid + lti * n_clusters) / p.n_groups;
+                const int64_t row0 = ((int64_t)mt * 2 + rank) * kBM;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int idx = tid + 64 * q;  // (row, chunk) = (idx / 8, idx % 8)
+                    const int64_t row = row0 + (idx >> 3);
+                    if (row < p.packed_rows) {
+                        const uint16_t* src = p.packed + row * p.k_pad + lkb * kBK + (idx & 7) * 8;
+                        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(v[q].x), "=r"(v[q].y), "=r"(v[q].z), "=r"(v[q].w)
+                                     : "l"(src));
+                    } else {
+                        v[q] = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                }
+            };
+            if (gsel < jobs) load_job(ti, kb);
+            PROF_BEGIN(3);
+            for (int j = gsel; j < jobs; j += kGroups) {
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                mbar_wait(&empty[stage], phase ^ 1u);
+                PROF_MARK(0);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int idx = tid + 64 * q;
+                    st_shared_v4(swz(sa, idx >> 3, (idx & 7) * 16), v[q]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                stage += kGroups;
+                while (stage >= S) { stage -= S; phase ^= 1u; }
+                kb += kGroups;
+                while (kb >= p.k_blocks) { kb -= p.k_blocks; ++ti; }
+                if (j + kGroups < jobs) load_job(ti, kb);
                 PROF_MARK(2);
             }
             if (cw == 0 && lane == 0) PROF_END(7, 3);
@@ -995,7 +1061,8 @@ struct pnce_plan {
                      // the whole grid does not hammer the same L2 lines in lock-step
     int num_sms;
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
-    Tiling packed;   // packed operand in: same grouping (A and B per-SM ingress, not the drain, bound G=256)
+    Tiling packed;   // packed operand via TMA: same grouping (TMA ingress, not the drain, bounds G=256)
+    Tiling packed_ldg;  // packed operand via LDG: <= 256 columns, double-buffered accumulator
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
 };
@@ -1104,7 +1171,10 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
     make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
     make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
-    p->rows_alloc = std::max(p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols);
+    const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
+    make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
+    p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
+                              p->packed_ldg.n_groups * p->packed_ldg.g_cols});
     p->num_sms = sms;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1142,6 +1212,9 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     if (s == PNCE_OK)
         s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
                       cfg->dtype == PNCE_DTYPE_BF16);
+    if (s == PNCE_OK)
+        s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2,
+                      cfg->dtype == PNCE_DTYPE_BF16);
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
         return s;
@@ -1156,6 +1229,9 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
                                             kSmemLimit);
         if (attr_err == cudaSuccess)
             attr_err = cudaFuncSetAttribute(k_correlate<kModeFusedTma>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmemLimit);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_correlate<kModePackedLdg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kSmemLimit);
     });
     if (attr_err != cudaSuccess) {
@@ -1212,6 +1288,33 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     return PNCE_OK;
 }
 
+// Diagnostic builds only: dump the cycle accounting / trace buffers after a launch.
+static void diag_dump(cudaStream_t st) {
+    (void)st;
+#ifdef PNCE_DIAG_PROF
+    if (const char* pf = std::getenv("PNCE_PROF_FILE")) {
+        static std::vector<unsigned long long> host(1024 * kProfSlots);
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host.data(), g_prof, host.size() * sizeof(unsigned long long));
+        if (FILE* fh = std::fopen(pf, "wb")) {
+            std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fh);
+            std::fclose(fh);
+        }
+    }
+#endif
+#ifdef PNCE_DIAG_TRACE
+    if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
+        static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(host.data(), g_trace, host.size() * sizeof(long long));
+        if (FILE* fh = std::fopen(tf, "wb")) {
+            std::fwrite(host.data(), sizeof(long long), host.size(), fh);
+            std::fclose(fh);
+        }
+    }
+#endif
+}
+
 static bool c_odd(const pnce_plan_t* p) { return (p->cfg.c & 1) != 0; }
 
 // Shared launch setup for both K3 variants.
@@ -1254,6 +1357,7 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.samples = c.c + c.m + c.l - 1;
     prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
     prm.inv_m = 1.0f / (float)c.m;
+    prm.k_pad = p->k_pad;
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
@@ -1273,17 +1377,33 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     if (n_frames == 0) return PNCE_OK;
     if (!packed || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
+    // packed operand: A with the circulant through TMA, one 512-column group (default), or
+    // LDG-fed A + double-buffered 256-column accumulators (PNCE_TUNE_PACKED_MODE=3; parity-
+    // green but 1.3x slower: one N=256 MMA per K-step cannot share A reads and the extra
+    // A stores push shared-memory bandwidth past the tensor rate)
+    const char* pm = std::getenv("PNCE_TUNE_PACKED_MODE");
+    const bool ldg = pm && std::atoi(pm) == kModePackedLdg;
+    const Tiling& t = ldg ? p->packed_ldg : p->packed;
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->packed, false, taps, truth, stats, n_frames, prm);
+    pnce_status_t s = fill_params(p, t, false, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
-    CUtensorMap tm_in;
     // packed rows: 2 per link, padded to whole 8-link blocks (a_row order)
     const uint64_t packed_rows = (uint64_t)((prm.total_links + 7) / 8) * 16;
-    s = make_tmap(&tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
-    if (s != PNCE_OK) return s;
-    const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-    k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, static_cast<cudaStream_t>(stream)>>>(
-        tm_in, p->packed.tm_circ, prm);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ldg) {
+        prm.packed = static_cast<const uint16_t*>(packed);
+        prm.packed_rows = (int64_t)packed_rows;
+        prm.tx_bytes = 2 * (uint32_t)(t.g_cols / 2) * kBK * 2;  // circulant only
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
+        k_correlate<kModePackedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(t.tm_circ, t.tm_circ, prm);
+    } else {
+        CUtensorMap tm_in;
+        s = make_tmap(&tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
+        if (s != PNCE_OK) return s;
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
+        k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_in, t.tm_circ, prm);
+    }
+    diag_dump(st);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;
@@ -1342,28 +1462,7 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(map_ok ? tm_raw : p->fused.tm_circ,
                                                                                    p->fused.tm_circ, prm);
     }
-#ifdef PNCE_DIAG_PROF
-    if (const char* pf = std::getenv("PNCE_PROF_FILE")) {
-        static std::vector<unsigned long long> host(1024 * kProfSlots);
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(host.data(), g_prof, host.size() * sizeof(unsigned long long));
-        if (FILE* fh = std::fopen(pf, "wb")) {
-            std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fh);
-            std::fclose(fh);
-        }
-    }
-#endif
-#ifdef PNCE_DIAG_TRACE
-    if (const char* tf = std::getenv("PNCE_TRACE_FILE")) {
-        static std::vector<long long> host(2 * kTraceSlots * kTraceMax);
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(host.data(), g_trace, host.size() * sizeof(long long));
-        if (FILE* fh = std::fopen(tf, "wb")) {
-            std::fwrite(host.data(), sizeof(long long), host.size(), fh);
-            std::fclose(fh);
-        }
-    }
-#endif
+    diag_dump(st);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     return PNCE_OK;

@@ -272,6 +272,24 @@ def test_fused_variants_agree(dev, mode, monkeypatch):
     assert link_err(taps.cpu().numpy(), oracle_est(chips, ocfg, iq)) <= TOL
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_packed_variants_agree(dev, monkeypatch, name):
+    """Packed operand through TMA (mode 0, 512-column group) == through LDG (mode 3,
+    256-column double-buffered groups), bit for bit, and within tolerance of the oracle."""
+    n, m, l, nb = CONFIGS[name]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    chips, iq, _ = sim_sets(ocfg, 2)
+    deg = (m + 1).bit_length() - 1
+    corr = P.Correlator(P.default_spec(deg), cfg, n, device=dev)
+    packed = corr.pack(torch.from_numpy(iq).to(dev))
+    via_tma, _ = corr.correlate(packed, 2)
+    monkeypatch.setenv("PNCE_TUNE_PACKED_MODE", "3")
+    via_ldg, _ = corr.correlate(packed, 2)
+    monkeypatch.delenv("PNCE_TUNE_PACKED_MODE")
+    assert torch.equal(via_tma, via_ldg)
+    assert link_err(via_ldg.cpu().numpy(), oracle_est(chips, ocfg, iq)) <= TOL
+
+
 def test_odd_row_stride(dev):
     """C + L odd -> odd samples per row (8-byte aligned rows): exercises the LDG path."""
     cfg, ocfg = make_cfg(16, 255, 32, 4, c=33)
