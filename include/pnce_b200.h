@@ -121,6 +121,15 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* plan, const float* iq, floa
                                   const float* truth, double* stats, void* workspace,
                                   size_t workspace_bytes, int64_t n_frames, void* stream);
 
+/* process_frames + fused per-link scoring (north star (4)): as pnce_process_frames,
+ * and when link_err != NULL (float32 [F][n_r][n_t], zeroed by the caller; needs truth)
+ * each entry receives the link's MSE, mean over its L taps of |h_est - h_true|^2,
+ * reduced in the epilogue with warp shuffles.  Reference: the mae/MSE scoring of
+ * metrics.py:19-25 applied per (r, t) link of CirEstimate.taps (estimator.py:27-37). */
+pnce_status_t pnce_process_frames_scored(const pnce_plan_t* plan, const float* iq, float* taps,
+                                         const float* truth, double* stats, float* link_err,
+                                         int64_t n_frames, void* stream);
+
 /* Launch-count accounting: number of device kernels this library has
  * launched in the calling process (for bench.py's gpu_launches). */
 int64_t pnce_kernel_launches(void);

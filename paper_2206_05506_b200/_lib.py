@@ -35,7 +35,8 @@ _STATUS = {
 EXPORTS = (
     "pnce_version", "pnce_last_error", "pnce_config_check", "pnce_generate_mseq",
     "pnce_plan_create", "pnce_plan_destroy", "pnce_plan_chips", "pnce_workspace_bytes",
-    "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_kernel_launches",
+    "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored",
+    "pnce_kernel_launches",
 )
 
 
@@ -76,6 +77,7 @@ def lib() -> ctypes.CDLL:
         "pnce_pack_iq": (i32, [vp, vp, vp, i64, vp]),
         "pnce_correlate": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames": (i32, [vp, vp, vp, vp, vp, vp, sz, i64, vp]),
+        "pnce_process_frames_scored": (i32, [vp, vp, vp, vp, vp, vp, i64, vp]),
         "pnce_kernel_launches": (i64, []),
     }
     for name, (res, args) in sig.items():

@@ -257,6 +257,8 @@ struct CorrParams {
     float* taps;
     const float* truth;
     double* stats;
+    float* link_err;  // optional [F][n_r][n_t]: mean_l |h_est - h_true|^2 per link (needs truth)
+    float inv_l;
 };
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
@@ -276,6 +278,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int byte_in_row)
 // Output window of one link (f, b, r) for the epilogue.
 struct EpiLink {
     int64_t out;      // complex index of lag 0 of the link's run in taps[f, r, t, l]; -1 = padding link
+    int64_t lbase;    // (f, r, first transmitter of the batch) index into link_err
     int64_t f;        // frame-set
     int n_valid;      // valid lags in the run (n_tx * L)
     bool vec;         // taps + 2*out is 16-byte aligned (pairs of lags as one 16-byte store)
@@ -286,35 +289,74 @@ __device__ __forceinline__ EpiLink make_link(const CorrParams& p, int64_t link) 
     EpiLink e;
     if (link >= p.total_links) {
         e.out = -1;
+        e.lbase = -1;
         e.f = -1;
         e.n_valid = 0;
         e.vec = e.tvec = false;
         return e;
     }
-    const int r = (int)(link % p.n_r);
-    const int64_t fb = link / p.n_r;
-    const int b = (int)(fb % p.n_batches);
-    e.f = fb / p.n_batches;
+    // links < 2^31 (checked on the host): 32-bit divisions
+    const uint32_t l32 = (uint32_t)link;
+    const uint32_t fb = l32 / (uint32_t)p.n_r;
+    const int r = (int)(l32 - fb * (uint32_t)p.n_r);
+    const uint32_t f32 = fb / (uint32_t)p.n_batches;
+    const int b = (int)(fb - f32 * (uint32_t)p.n_batches);
+    e.f = f32;
     const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
     e.n_valid = n_tx * p.l;
-    e.out = ((e.f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch) * p.l;
+    e.lbase = (e.f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch;
+    e.out = e.lbase * p.l;
     e.vec = (reinterpret_cast<uintptr_t>(p.taps + 2 * e.out) & 15) == 0;
     e.tvec = p.truth != nullptr && (reinterpret_cast<uintptr_t>(p.truth + 2 * e.out) & 15) == 0;
     return e;
 }
 
-__device__ __forceinline__ void err_acc(float re, float im, float hr, float hi, float& s_abs, float& s_sq) {
+__device__ __forceinline__ float err_acc(float re, float im, float hr, float hi, float& s_abs, float& s_sq) {
     const float dx = re - hr, dy = im - hi;
     const float sq = dx * dx + dy * dy;
     s_sq += sq;
-    s_abs += sqrtf(sq);
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sq));  // MAE term: ~1 ulp is plenty
+    s_abs += r;
+    return sq;
+}
+
+// Per-link (per transmitter window) squared-error partial of one thread.  A thread's lags
+// increase monotonically, so windows are visited in order: flush when a lag crosses the
+// next window boundary.  `quad`: L % 8 == 0, so the four lanes of a link cross together
+// (warp-uniform) and reduce with two shuffles before one atomic; otherwise each lane
+// flushes on its own.
+struct LinkAcc {
+    int w;       // current window (transmitter within the batch)
+    int next;    // first lag of window w + 1
+    float part;
+};
+
+__device__ __forceinline__ void link_flush(const CorrParams& p, const EpiLink& e, LinkAcc& a, bool quad) {
+    float v = a.part;
+    if (quad) {
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+    }
+    if ((!quad || (threadIdx.x & 3) == 0) && e.out >= 0 && a.w >= 0 && v != 0.f)
+        atomicAdd(p.link_err + e.lbase + a.w, v * p.inv_l);
+    a.part = 0.f;
+}
+
+__device__ __forceinline__ void link_add(const CorrParams& p, const EpiLink& e, LinkAcc& a, int lag, float sq) {
+    if (lag >= a.next) {
+        link_flush(p, e, a, false);
+        a.w = lag / p.l;
+        a.next = (a.w + 1) * p.l;
+    }
+    a.part += sq;
 }
 
 // K4 for R repetitions of a 16x256b TMEM load: repetition i holds, for this thread's link,
 // Re (v[4i], v[4i+1]) and Im (v[4i+2], v[4i+3]) of lags n + 8i and n + 8i + 1.
-template <int R>
+template <int R, bool SC>
 __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v, const EpiLink& e, int n,
-                                         float& s_abs, float& s_sq, float& nf) {
+                                         float& s_abs, float& s_sq, float& nf, LinkAcc& la) {
 #pragma unroll
     for (int i = 0; i < R; ++i) {
         const int lag = n + 8 * i;
@@ -323,7 +365,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
         const float im0 = __uint_as_float(v[4 * i + 2]) * p.inv_m;
         const float im1 = __uint_as_float(v[4 * i + 3]) * p.inv_m;
         if (e.out < 0 || lag >= e.n_valid) continue;
-        if (p.stats != nullptr) {
+        if (SC && p.stats != nullptr) {
             // sticky non-finite detector (inf * 0 = NaN); exact count only when it fires
             nf = fmaf(re0, 0.f, nf);
             nf = fmaf(im0, 0.f, nf);
@@ -335,7 +377,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
         float* dst = p.taps + 2 * (e.out + lag);
         const float* tr = p.truth + 2 * (e.out + lag);
         if (lag + 1 < e.n_valid) {
-            if (p.stats != nullptr) {
+            if (SC && p.stats != nullptr) {
                 nf = fmaf(re1, 0.f, nf);
                 nf = fmaf(im1, 0.f, nf);
             }
@@ -345,7 +387,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
                 *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
                 *reinterpret_cast<float2*>(dst + 2) = make_float2(re1, im1);
             }
-            if (p.truth != nullptr) {
+            if (SC && p.truth != nullptr) {
                 float4 h;
                 if (e.tvec) {
                     h = ld_global_nc_v4(tr);
@@ -354,14 +396,19 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
                     const float2 b = __ldg(reinterpret_cast<const float2*>(tr) + 1);
                     h = make_float4(a.x, a.y, b.x, b.y);
                 }
-                err_acc(re0, im0, h.x, h.y, s_abs, s_sq);
-                err_acc(re1, im1, h.z, h.w, s_abs, s_sq);
+                const float q0 = err_acc(re0, im0, h.x, h.y, s_abs, s_sq);
+                const float q1 = err_acc(re1, im1, h.z, h.w, s_abs, s_sq);
+                if (p.link_err != nullptr) {
+                    link_add(p, e, la, lag, q0);
+                    link_add(p, e, la, lag + 1, q1);
+                }
             }
         } else {
             *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
-            if (p.truth != nullptr) {
+            if (SC && p.truth != nullptr) {
                 const float2 a = __ldg(reinterpret_cast<const float2*>(tr));
-                err_acc(re0, im0, a.x, a.y, s_abs, s_sq);
+                const float q0 = err_acc(re0, im0, a.x, a.y, s_abs, s_sq);
+                if (p.link_err != nullptr) link_add(p, e, la, lag, q0);
             }
         }
     }
@@ -370,10 +417,12 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
 // Drain one 16-lane block (8 links) of the accumulator: TMEM -> x 1/M -> taps (+ scoring).
 // 64-column chunks double-buffered (the next chunk's TMEM load is in flight while the
 // current one is scaled and stored), then 16-column remainder pieces.
+template <bool SC>
 __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
                                           float& s_abs, float& s_sq, float& nf) {
     const int cols = p.g_cols;
     int c = 0;
+    LinkAcc la{-1, 0, 0.f};
     uint32_t va[32], vb[32];
     if (cols >= 64) {
         tmem_ld_16x256b_x8(taddr, va);
@@ -381,13 +430,13 @@ __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, c
         while (true) {
             const bool more = c + 128 <= cols;
             if (more) tmem_ld_16x256b_x8(taddr + c + 64, vb);
-            epi_reps<8>(p, va, e, n0 + c, s_abs, s_sq, nf);
+            epi_reps<8, SC>(p, va, e, n0 + c, s_abs, s_sq, nf, la);
             c += 64;
             if (!more) break;
             tmem_wait_ld();
             const bool more2 = c + 128 <= cols;
             if (more2) tmem_ld_16x256b_x8(taddr + c + 64, va);
-            epi_reps<8>(p, vb, e, n0 + c, s_abs, s_sq, nf);
+            epi_reps<8, SC>(p, vb, e, n0 + c, s_abs, s_sq, nf, la);
             c += 64;
             if (!more2) break;
             tmem_wait_ld();
@@ -397,8 +446,99 @@ __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, c
         uint32_t v[8];
         tmem_ld_16x256b_x2(taddr + c, v);
         tmem_wait_ld();
-        epi_reps<2>(p, v, e, n0 + c, s_abs, s_sq, nf);
+        epi_reps<2, SC>(p, v, e, n0 + c, s_abs, s_sq, nf, la);
     }
+    if (SC && p.link_err != nullptr) link_flush(p, e, la, false);
+}
+
+// Scored drain (truth present, g_cols % 32 == 0): 32-column chunks; the truth of chunk k+1
+// is loaded while chunk k is processed (two register buffers), after the whole tile's
+// truth was pulled into L2 during the main loop.  Per-link errors reduce over the lane quad.
+__device__ __forceinline__ void load_truth4(const CorrParams& p, const EpiLink& e, int lag0, float4 (&h)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int lag = lag0 + 8 * i;
+        const float* tr = p.truth + 2 * (e.out + lag);
+        if (e.out >= 0 && lag + 1 < e.n_valid && e.tvec) {
+            h[i] = ld_global_nc_v4(tr);
+        } else if (e.out >= 0 && lag < e.n_valid) {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(tr));
+            const float2 b = lag + 1 < e.n_valid ? __ldg(reinterpret_cast<const float2*>(tr) + 1) : make_float2(0.f, 0.f);
+            h[i] = make_float4(a.x, a.y, b.x, b.y);
+        } else {
+            h[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
+__device__ __forceinline__ void epi_reps_scored(const CorrParams& p, const uint32_t (&v)[16], const float4 (&h)[4],
+                                                const EpiLink& e, int n, float& s_abs, float& s_sq, float& nf,
+                                                LinkAcc& la, bool quad) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int lag = n + 8 * i;
+        if (p.link_err != nullptr && quad && lag >= la.next) {  // warp-uniform when quad
+            link_flush(p, e, la, true);
+            la.w = lag / p.l;
+            la.next = (la.w + 1) * p.l;
+        }
+        const float re0 = __uint_as_float(v[4 * i + 0]) * p.inv_m;
+        const float re1 = __uint_as_float(v[4 * i + 1]) * p.inv_m;
+        const float im0 = __uint_as_float(v[4 * i + 2]) * p.inv_m;
+        const float im1 = __uint_as_float(v[4 * i + 3]) * p.inv_m;
+        if (e.out < 0 || lag >= e.n_valid) continue;
+        nf = fmaf(re0, 0.f, nf);
+        nf = fmaf(im0, 0.f, nf);
+        float* dst = p.taps + 2 * (e.out + lag);
+        const float q0 = err_acc(re0, im0, h[i].x, h[i].y, s_abs, s_sq);
+        if (lag + 1 < e.n_valid) {
+            nf = fmaf(re1, 0.f, nf);
+            nf = fmaf(im1, 0.f, nf);
+            if (e.vec) {
+                st_global_v4(dst, re0, im0, re1, im1);
+            } else {
+                *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+                *reinterpret_cast<float2*>(dst + 2) = make_float2(re1, im1);
+            }
+            const float q1 = err_acc(re1, im1, h[i].z, h[i].w, s_abs, s_sq);
+            if (p.link_err != nullptr) {
+                if (quad) {
+                    la.part += q0 + q1;
+                } else {
+                    link_add(p, e, la, lag, q0);
+                    link_add(p, e, la, lag + 1, q1);
+                }
+            }
+        } else {
+            *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+            if (p.link_err != nullptr) {
+                if (quad) la.part += q0;
+                else link_add(p, e, la, lag, q0);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void epi_block_scored(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
+                                                 float& s_abs, float& s_sq, float& nf) {
+    const int cols = p.g_cols;  // multiple of 32 here
+    const bool quad = (p.l & 7) == 0;
+    LinkAcc la{-1, 0, 0.f};
+    float4 h0[4], h1[4];
+    uint32_t v[16];
+    int c = 0;
+    load_truth4(p, e, n0, h0);
+    auto step = [&](float4 (&hc)[4], float4 (&hn)[4]) -> bool {
+        tmem_ld_16x256b_x4(taddr + c, v);
+        if (c + 32 < cols) load_truth4(p, e, n0 + c + 32, hn);
+        tmem_wait_ld();
+        epi_reps_scored(p, v, hc, e, n0 + c, s_abs, s_sq, nf, la, quad);
+        c += 32;
+        return c < cols;
+    };
+    while (step(h0, h1) && step(h1, h0)) {
+    }
+    if (p.link_err != nullptr) link_flush(p, e, la, quad);
 }
 
 // Fast drain of one 16-lane block when every lag this thread owns is valid, the run is
@@ -477,7 +617,7 @@ __device__ __forceinline__ void prefetch_raw_chunk(const CorrParams& p, const CU
     tma_prefetch_l2_2d(tm, (2 * (p.c + kb * kBK + (jc & 1) * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile);
 }
 
-template <int MODE>
+template <int MODE, bool SCORED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
@@ -486,9 +626,14 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     constexpr bool FLDG = MODE == kModeFusedLdg;    // f32 rows LDG'd, converted
     constexpr bool PLDG = MODE == kModePackedLdg;   // packed 16-bit rows LDG'd
     constexpr bool FUSED = RAW || FLDG;
+    // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
+    // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
+    constexpr int kCW = (SCORED && RAW) ? 4 : kConvWarps;
+    constexpr int kEW0 = kConvWarp0 + kCW;
+    constexpr int kEW = kWarps - kEW0;
     // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
     // one 2-warp group (PLDG)
-    constexpr int kConvArrivals = RAW ? 2 * kConvWarps : (FLDG ? kConvWarps : (PLDG ? kConvWarps / 2 : 0));
+    constexpr int kConvArrivals = RAW ? 2 * kCW : (FLDG ? kConvWarps : (PLDG ? kConvWarps / 2 : 0));
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -518,12 +663,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * kEpiWarps);
+            mbar_init(&tempty[a], 2 * kEW);
         }
         if (RAW) {
             for (int s = 0; s < p.raw_stages; ++s) {
                 mbar_init(&raw_full[s], 1);
-                mbar_init(&raw_empty[s], kConvWarps);
+                mbar_init(&raw_empty[s], kCW);
             }
         }
         fence_mbar_init();
@@ -691,7 +836,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             }
             PROF_END(5, 2);
         }
-    } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kConvWarps) {
+    } else if (warp >= kConvWarp0 && warp < kEW0) {
         if (RAW) {
             const int cw = warp - kConvWarp0;
             int kb = 0, stage = 0, rs = 0;
@@ -719,8 +864,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         const int col_byte = h * 64 + (lane & 15) * 4;
 #ifndef PNCE_DIAG_NO_CONV
 #pragma unroll
-                        for (int it = 0; it < kLinksPerTile / (2 * kConvWarps); ++it) {
-                            const int idx = cw + kConvWarps * it;  // 0..31
+                        for (int it = 0; it < kLinksPerTile / (2 * kCW); ++it) {
+                            const int idx = cw + kCW * it;  // 0..31
                             const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
                             const uint32_t src = raw + link * (p.raw_row_floats * 4);
                             float4 v;
@@ -876,11 +1021,14 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             }
             if (cw == 0 && lane == 0) PROF_END(7, 3);
         }
-    } else if (warp >= kEpiWarp0) {
+    } else if (warp >= kEW0) {
         // ===== epilogue (both CTAs): warp q = warp % 4 owns TMEM lanes 32q..32q+31 = two
         // 16-row blocks = links 16q..16q+15 of this CTA's 64; thread t handles link
         // 8*block + t/4 of its quarter and lags 2(t%4), 2(t%4)+1 of every 8-lag repetition.
         const int quarter = warp & 3;
+        // 4 epilogue warps: each drains both 16-lane blocks of its quarter; 8 (scored): one
+        constexpr int kBlocksPerWarp = kEW == 4 ? 2 : 1;
+        const int bb0 = kEW == 4 ? 0 : (warp - kEW0) >> 2;
         const int colp = 2 * (lane & 3);
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
@@ -891,13 +1039,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int mt = tile / p.n_groups;
             const int g = tile - mt * p.n_groups;
             const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
-            const EpiLink e0 = make_link(p, link0);
-            const EpiLink e1 = make_link(p, link0 + 8);
+            // (links are re-derived where needed instead of kept live: register pressure)
             const int n0 = g * p.g_cols + colp;
-            if (p.truth != nullptr && (lane & 3) == 0) {
+            if (SCORED && p.truth != nullptr && (lane & 3) == 0) {
                 // pull this tile's truth windows into L2 while the MMAs run
-                for (int bb = 0; bb < 2; ++bb) {
-                    const EpiLink& e = bb ? e1 : e0;
+                for (int k = 0; k < kBlocksPerWarp; ++k) {
+                    const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
                     const int lag0 = g * p.g_cols;
                     const int n = min(p.g_cols, e.n_valid - lag0);
                     if (e.out >= 0 && n > 0) {
@@ -909,42 +1056,59 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     }
                 }
             }
+            // plain drain: decide the fast path and its output pointer before the wait
+            float* fast_dst[2] = {nullptr, nullptr};
+            if constexpr (!SCORED) {
+#pragma unroll
+                for (int k = 0; k < kBlocksPerWarp; ++k) {
+                    const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
+                    const bool ok = __all_sync(0xffffffffu, e.out >= 0 && e.vec && g * p.g_cols + p.g_cols <= e.n_valid);
+                    fast_dst[k] = ok ? p.taps + 2 * (e.out + n0) : nullptr;
+                }
+            }
             mbar_wait(&tfull[acc], acc_phase);
             PROF_MARK(0);
-            if (lane == 0 && warp == kEpiWarp0) TRACE(10, ti);
+            if (lane == 0 && warp == kEW0) TRACE(10, ti);
             tc_fence_after();
 
             float s_abs[2] = {0.f, 0.f}, s_sq[2] = {0.f, 0.f}, nf[2] = {0.f, 0.f};
             const uint32_t t_acc = tmem_base + (uint32_t)(acc * p.g_cols);
-            const bool plain = p.stats == nullptr;  // no scoring: fast path where the window allows
 #pragma unroll
-            for (int bb = 0; bb < 2; ++bb) {
-                const EpiLink& e = bb ? e1 : e0;
+            for (int k = 0; k < kBlocksPerWarp; ++k) {
+                const int bb = bb0 + k;
                 const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16);
-                // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
-                const bool fast = __all_sync(0xffffffffu, plain && e.out >= 0 && e.vec &&
-                                                              g * p.g_cols + p.g_cols <= e.n_valid);
-                if (fast)
-                    epi_block_fast(p, taddr, p.taps + 2 * (e.out + n0));
-                else
-                    epi_block(p, taddr, e, n0, s_abs[bb], s_sq[bb], nf[bb]);
+                if constexpr (SCORED) {
+                    const EpiLink e = make_link(p, link0 + 8 * bb);
+                    if (p.truth != nullptr && (p.g_cols & 31) == 0)
+                        epi_block_scored(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
+                    else
+                        epi_block<true>(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
+                } else {
+                    // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
+                    if (fast_dst[k] != nullptr) {
+                        epi_block_fast(p, taddr, fast_dst[k]);
+                    } else {
+                        const EpiLink e = make_link(p, link0 + 8 * bb);
+                        epi_block<false>(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
+                    }
+                }
             }
             // this warp's share of the accumulator is drained -> tell the leader's MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
-            if (lane == 0 && warp == kEpiWarp0) TRACE(11, ti);
-            if (lane == 0 && warp == kEpiWarp0 + kEpiWarps - 1) TRACE(12, ti);
+            if (lane == 0 && warp == kEW0) TRACE(11, ti);
+            if (lane == 0 && warp == kWarps - 1) TRACE(12, ti);
             if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             PROF_MARK(1);
 
-            if (p.stats != nullptr) {
+            if (SCORED && p.stats != nullptr) {
 #pragma unroll
-                for (int bb = 0; bb < 2; ++bb) {
-                    const EpiLink& e = bb ? e1 : e0;
+                for (int k = 0; k < kBlocksPerWarp; ++k) {
+                    const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
                     float bad = 0.f;
-                    if (e.out >= 0 && nf[bb] != 0.f) bad = recount_nonfinite(p, e, n0);
-                    float sa = s_abs[bb], sq = s_sq[bb];
+                    if (e.out >= 0 && nf[k] != 0.f) bad = recount_nonfinite(p, e, n0);
+                    float sa = s_abs[k], sq = s_sq[k];
                     // per-frame reduction: warp-uniform frame -> one atomic per warp.  Links
                     // ascend with the lane, so lane 0 holds the block's first (valid) link.
                     const bool lead_ok = __shfl_sync(0xffffffffu, e.out >= 0, 0);
@@ -974,7 +1138,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
             }
         }
-        if (warp == kEpiWarp0 && lane == 0) PROF_END(10, 2);
+        if (warp == kEW0 && lane == 0) PROF_END(10, 2);
     }
 
     __syncwarp();
@@ -1086,6 +1250,25 @@ static void make_tiling(Tiling& t, int r_total, int max_group) {
     uint32_t cols = 32;
     while (cols < (uint32_t)(t.acc_stages * g)) cols <<= 1;
     t.tmem_cols = cols;
+}
+
+template <int MODE>
+static cudaError_t set_smem_attrs() {
+    cudaError_t e = cudaFuncSetAttribute(k_correlate<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_correlate<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    return e;
+}
+
+// Scored variants (truth / stats / per-link errors) are separate instantiations so the
+// plain drain keeps its registers.
+template <int MODE>
+static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
+                      const CUtensorMap& b, const CorrParams& prm) {
+    if (scored)
+        k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+    else
+        k_correlate<MODE, false><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
 }
 
 extern "C" {
@@ -1222,17 +1405,10 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(k_correlate<kModePacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kSmemLimit);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_correlate<kModeFusedLdg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kSmemLimit);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_correlate<kModeFusedTma>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kSmemLimit);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_correlate<kModePackedLdg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            kSmemLimit);
+        attr_err = set_smem_attrs<kModePacked>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedLdg>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedTma>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModePackedLdg>();
     });
     if (attr_err != cudaSuccess) {
         pnce_plan_destroy(p);
@@ -1357,6 +1533,7 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.samples = c.c + c.m + c.l - 1;
     prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
     prm.inv_m = 1.0f / (float)c.m;
+    prm.inv_l = 1.0f / (float)c.l;
     prm.k_pad = p->k_pad;
     prm.taps = taps;
     prm.truth = truth;
@@ -1395,13 +1572,13 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
         prm.packed_rows = (int64_t)packed_rows;
         prm.tx_bytes = 2 * (uint32_t)(t.g_cols / 2) * kBK * 2;  // circulant only
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        k_correlate<kModePackedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(t.tm_circ, t.tm_circ, prm);
+        launch_k3<kModePackedLdg>(truth || stats, pair_grid(p, prm), smem, st, t.tm_circ, t.tm_circ, prm);
     } else {
         CUtensorMap tm_in;
         s = make_tmap(&tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
         if (s != PNCE_OK) return s;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        k_correlate<kModePacked><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_in, t.tm_circ, prm);
+        launch_k3<kModePacked>(truth || stats, pair_grid(p, prm), smem, st, tm_in, t.tm_circ, prm);
     }
     diag_dump(st);
     g_launches++;
@@ -1409,11 +1586,28 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     return PNCE_OK;
 }
 
+static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                         double* stats, float* link_err, int64_t n_frames, void* stream);
+
 pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                   double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
                                   void* stream) {
     (void)workspace;
     (void)workspace_bytes;
+    return process_frames_impl(p, iq, taps, truth, stats, nullptr, n_frames, stream);
+}
+
+pnce_status_t pnce_process_frames_scored(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                         double* stats, float* link_err, int64_t n_frames, void* stream) {
+    if (link_err && !truth) return fail(PNCE_ERR_INVALID_CONFIG, "per-link errors need the ground truth");
+    if (reinterpret_cast<uintptr_t>(link_err) & 3) return fail(PNCE_ERR_DIMENSION, "link_err must be 4-byte aligned");
+    return process_frames_impl(p, iq, taps, truth, stats, link_err, n_frames, stream);
+}
+
+}  // extern "C"
+
+static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                         double* stats, float* link_err, int64_t n_frames, void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
@@ -1423,6 +1617,8 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     pnce_status_t s = fill_params(p, p->fused, true, taps, truth, stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
+    prm.link_err = link_err;
+    const bool scored = truth || stats || link_err;
     const int samples = prm.samples;
     const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
     // the raw f32 rows can be described by a tensor map when the row stride is 16-byte aligned
@@ -1454,13 +1650,13 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
         prm.raw_stages = raw;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
                             (size_t)prm.raw_stages * prm.raw_stage_bytes;
-        k_correlate<kModeFusedTma><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(tm_raw, p->fused.tm_circ, prm);
+        launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, p->fused.tm_circ, prm);
     } else {
         if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         // tm_in (the raw map) only serves the L2 prefetcher in the LDG variant
-        k_correlate<kModeFusedLdg><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(map_ok ? tm_raw : p->fused.tm_circ,
-                                                                                   p->fused.tm_circ, prm);
+        launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, map_ok ? tm_raw : p->fused.tm_circ,
+                                 p->fused.tm_circ, prm);
     }
     diag_dump(st);
     g_launches++;
@@ -1468,4 +1664,4 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     return PNCE_OK;
 }
 
-}  // extern "C"
+

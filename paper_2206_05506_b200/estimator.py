@@ -31,7 +31,8 @@ class CirEstimate:
     """estimator.py:27-37.  taps: complex64 device tensor (n_r, n_t, L) or (F, n_r, n_t, L).
 
     ``stats`` (float64 (F, 4): sum|e|, sum|e|^2, non-finite count, 0) is filled
-    by the fused epilogue when ground truth was supplied.
+    by the fused epilogue when ground truth was supplied, and ``link_mse``
+    (float32 (F, n_r, n_t) or (n_r, n_t)) with each link's mean |e|^2 over its L taps.
     """
 
     taps: torch.Tensor
@@ -39,6 +40,7 @@ class CirEstimate:
     norm: float
     saturations: int = 0
     stats: torch.Tensor | None = None
+    link_mse: torch.Tensor | None = None
 
     def mae(self) -> float:
         """metrics.py:19-25 from the fused per-frame sums."""
@@ -186,6 +188,35 @@ class Correlator:
                 truth_ptr, stats_ptr, None, 0, n_frames, _stream_ptr(self.device)))
         return out, stats
 
+    def process_scored(self, iq: torch.Tensor, truth: torch.Tensor, out: torch.Tensor | None = None,
+                       stats: torch.Tensor | None = None, link_mse: torch.Tensor | None = None):
+        """`process` with the fused per-link scoring (north star (4)): returns
+        (taps, stats (F, 4) f64, link_mse (F, n_r, n_t) f32 = mean_l |h_est - h_true|^2)."""
+        iq, n_frames = self._check_iq(iq)
+        if out is None:
+            out = torch.empty(self.taps_shape(n_frames), dtype=torch.complex64, device=self.device)
+        elif tuple(out.shape) != self.taps_shape(n_frames) or out.dtype != torch.complex64 or not out.is_contiguous():
+            raise DimensionMismatchError("out must be contiguous complex64 (F, n_r, n_t, L)")
+        if truth is None or tuple(truth.shape) != self.taps_shape(n_frames) or truth.dtype != torch.complex64 \
+                or not truth.is_cuda:
+            raise DimensionMismatchError("truth must be CUDA complex64 (F, n_r, n_t, L)")
+        truth = truth.contiguous()
+        if stats is None:
+            stats = torch.zeros((n_frames, 4), dtype=torch.float64, device=self.device)
+        elif tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64:
+            raise DimensionMismatchError("stats must be float64 (F, 4)")
+        lshape = (n_frames, self.n_r, self.cfg.n_t)
+        if link_mse is None:
+            link_mse = torch.zeros(lshape, dtype=torch.float32, device=self.device)
+        elif tuple(link_mse.shape) != lshape or link_mse.dtype != torch.float32 or not link_mse.is_contiguous():
+            raise DimensionMismatchError("link_mse must be contiguous float32 (F, n_r, n_t), zero-filled")
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().pnce_process_frames_scored(
+                self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                ctypes.c_void_p(truth.data_ptr()), ctypes.c_void_p(stats.data_ptr()),
+                ctypes.c_void_p(link_mse.data_ptr()), n_frames, _stream_ptr(self.device)))
+        return out, stats, link_mse
+
     def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64) -> torch.Tensor:
         """Host-buffer path (IQ ingest): pinned host IQ -> HBM by chunked
         async copies on a copy stream, pack + correlate on the current stream, taps back
@@ -330,7 +361,11 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
         truth_t = truth_t.to(device=corr.device, dtype=torch.complex64)
         if truth_t.dim() == 3:
             truth_t = truth_t.unsqueeze(0)
-    taps, stats = corr.process(iq, truth=truth_t)
+    link_mse = None
+    if truth_t is not None:
+        taps, stats, link_mse = corr.process_scored(iq, truth_t)
+    else:
+        taps, stats = corr.process(iq)
     n_frames = taps.shape[0]
     if counters is not None:
         counters.samples_moved += n_frames * cfg.n_batches * n_r * cfg.p
@@ -339,5 +374,7 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
     saturations = 0
     if stats is not None:
         saturations = int(stats[:, 2].sum().item())
+    if link_mse is not None and single:
+        link_mse = link_mse[0]
     return CirEstimate(taps=out_taps, backend=f"tcgen05-{dtype}", norm=1.0 / cfg.m,
-                       saturations=saturations, stats=stats)
+                       saturations=saturations, stats=stats, link_mse=link_mse)

@@ -290,6 +290,67 @@ def test_packed_variants_agree(dev, monkeypatch, name):
     assert link_err(via_ldg.cpu().numpy(), oracle_est(chips, ocfg, iq)) <= TOL
 
 
+LINK_CASES = [("cfg2", None), ("cfg3", None), ("cfg4p", None), ("odd_l", (5, 3, 255, 20, 20, 5)),
+              ("l127", (16, 2, 1023, 127, 127, 8))]
+
+
+@pytest.mark.parametrize("name,layout", LINK_CASES)
+def test_link_mse_fused(dev, name, layout):
+    """Per-link MSE from the fused epilogue (north star (4)) == mean_l |h_est - h|^2 of the
+    written taps; frame sums agree with the per-link values; quad (L % 8 == 0) and per-lane
+    (odd L) reductions both covered."""
+    if layout is None:
+        n, m, l, nb = CONFIGS[name]
+        cfg, ocfg = make_cfg(n, m, l, nb)
+        n_r = n
+    else:
+        n, n_r, m, l, c, nb = layout
+        cfg, ocfg = make_cfg(n, m, l, nb, n_r=n_r, c=c)
+    chips, iq, truth = sim_sets(ocfg, 2)
+    deg = (m + 1).bit_length() - 1
+    corr = P.Correlator(P.default_spec(deg), cfg, n_r, device=dev)
+    h = torch.from_numpy(truth.astype(np.complex64)).to(dev)
+    taps, stats, link = corr.process_scored(torch.from_numpy(iq).to(dev), h)
+    e2 = (taps - h).abs().double() ** 2
+    want = e2.mean(dim=-1)
+    got = link.double()
+    assert torch.allclose(got, want, rtol=1e-4, atol=1e-12)
+    # frame sums: sum|e|^2 over the frame == L * sum of the per-link means
+    assert torch.allclose(stats[:, 1], e2.sum(dim=(1, 2, 3)), rtol=1e-4)
+    assert torch.allclose(stats[:, 1], got.sum(dim=(1, 2)) * cfg.l, rtol=1e-4)
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_scored_modes_agree(dev, monkeypatch, mode):
+    """Scored drains of both converter modes (TMA-staged: 8 epilogue warps; LDG: 4) give
+    the same taps bit for bit and the same sums to rounding."""
+    n, m, l, nb = CONFIGS["cfg3"]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    _, iq, truth = sim_sets(ocfg, 2)
+    corr = P.Correlator(P.default_spec(10), cfg, n, device=dev)
+    x = torch.from_numpy(iq).to(dev)
+    h = torch.from_numpy(truth.astype(np.complex64)).to(dev)
+    plain, _ = corr.process(x)
+    monkeypatch.setenv("PNCE_TUNE_FUSED_MODE", mode)
+    taps, stats, link = corr.process_scored(x, h)
+    monkeypatch.delenv("PNCE_TUNE_FUSED_MODE")
+    assert torch.equal(taps, plain)
+    e2 = (taps - h).abs().double() ** 2
+    assert torch.allclose(link.double(), e2.mean(dim=-1), rtol=1e-4, atol=1e-12)
+    assert torch.allclose(stats[:, 0], (taps - h).abs().double().sum(dim=(1, 2, 3)), rtol=1e-4)
+
+
+def test_link_mse_front_end(dev):
+    """process_frames(truth=...) returns CirEstimate.link_mse; MSE curve helpers agree."""
+    n, m, l, nb = CONFIGS["cfg2"]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    chips, iq, truth = sim_sets(ocfg, 1)
+    seq = P.sequence_for_length(m, dev)
+    est = P.process_frames(seq, cfg, P.build_batch_plan(cfg), torch.from_numpy(iq[0]).to(dev), truth=truth[0])
+    assert est.link_mse is not None and tuple(est.link_mse.shape) == (n, n)
+    assert abs(float(est.link_mse.double().mean()) - est.mse()) <= 1e-4 * est.mse()
+
+
 def test_odd_row_stride(dev):
     """C + L odd -> odd samples per row (8-byte aligned rows): exercises the LDG path."""
     cfg, ocfg = make_cfg(16, 255, 32, 4, c=33)
