@@ -98,6 +98,14 @@ class ClockSampler:
             self.thread.join(timeout=2)
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        limit = None
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=power.limit",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            limit = float(out.stdout.strip().splitlines()[0])
+        except Exception:
+            pass
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
@@ -107,7 +115,8 @@ class ClockSampler:
         loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": limit}
 
 
 def synth_iq_pool(corr, n_pool, w, seed, dev):
@@ -367,6 +376,37 @@ def run_gpu(args, rank, world):
                "h2d_bytes_per_step": host_iq.numel() * 4, "d2h_bytes_per_step": host_taps.numel() * 8,
                "frames_per_step": Fe, "us_per_frame": te / (Fe * reps) * 1e6}
 
+    # --- IQ-file ingest: reference-format file -> pinned chunks -> HBM ->
+    # taps in pinned host memory (the file is written untimed to a local temp dir and read
+    # back from the page cache)
+    ingest = None
+    if not args.no_e2e and args.file_frames > 0:
+        import tempfile
+        from paper_2206_05506_b200 import iqfile as IQ
+        Ff = min(args.file_frames, F)
+        hdr = IQ.IqFileHeader(n_t=w["n_t"], n_r=w["n_r"], p=w["c"] + w["m"], l=w["l"], m=w["m"], c=w["c"],
+                              n_batch=w["n_batch"], frame_count=Ff * corr.cfg.n_batches, seed=1234 + rank)
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "frames.iq")
+            IQ.write_iq_tensor(path, hdr, iq[:Ff])
+            taps_f = torch.empty(corr.taps_shape(Ff), dtype=torch.complex64).pin_memory()
+            IQ.estimate_file(path, corr, taps_host=taps_f)            # warm-up (page cache, pools)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            IQ.estimate_file(path, corr, taps_host=taps_f)
+            tf = time.perf_counter() - t0                               # host wall clock (file I/O)
+            ok = torch.equal(taps_f[:min(Ff, 4)], taps[:min(Ff, 4)].cpu())
+            if world > 1:
+                tt = torch.tensor([tf], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                tf = float(tt.item())
+            ingest = {"value": Ff * world / tf * w["n_r"] * w["n_t"], "unit": "CSI estimates/s",
+                      "frames": Ff, "file_bytes": os.path.getsize(path), "us_per_frame": tf / Ff * 1e6,
+                      "GB_per_s": os.path.getsize(path) / tf / 1e9, "taps_match_resident_path": bool(ok),
+                      "timing": "host wall clock, file in page cache"}
+            del taps_f
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, cores, sample, _ = cpu_reference_rate(w, seconds=args.cpu_seconds)
@@ -394,7 +434,7 @@ def run_gpu(args, rank, world):
                                          "frames_per_launch": F}},
             "gemm_leg": gemm,
             "estimate_quality": quality,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "ingest_iq_file": ingest, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -409,6 +449,7 @@ def main():
     ap.add_argument("--frames", type=int, default=10000, help="frame-sets per step per GPU")
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--e2e-frames", type=int, default=512)
+    ap.add_argument("--file-frames", type=int, default=256, help="frame-sets in the IQ-file ingest leg (0: off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gemm-leg", action="store_true")
