@@ -119,42 +119,6 @@ class ClockSampler:
                 "power_w": statistics.median(pw) if pw else None, "power_limit_w": limit}
 
 
-def synth_iq_pool(corr, n_pool, w, seed, dev):
-    """Statistically equivalent synthetic received IQ on the device (input synthesis only,
-    not timed): per-link channels with the draw_channel law (channel.py:96-108), the
-    noiseless CP-stripped body H.A (the circulant rows of the plan's own chips), CP =
-    body tail, AWGN at the configured SNR (channel.py:145-183)."""
-    import torch
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    n_t, n_r, l, m, c, nb = w["n_t"], w["n_r"], w["l"], w["m"], w["c"], w["n_batch"]
-    n_batches = -(-n_t // nb)
-    chips = corr.chips().double()
-    spacing = m // nb
-    lags = torch.tensor([(spacing * j + q) % m for j in range(nb) for q in range(l)], device=dev)
-    idx = (torch.arange(m, device=dev)[None, :] - lags[:, None]) % m
-    A = chips[idx]                                           # (nb*L, M)
-    amax = math.sqrt(1.0 / (n_t * math.sqrt(l)))
-    amp = amax * (1.0 - torch.rand((n_pool, n_r, n_t, l), generator=g, device=dev, dtype=torch.float64))
-    ph = 2 * math.pi * torch.rand((n_pool, n_r, n_t, l), generator=g, device=dev, dtype=torch.float64)
-    h = torch.polar(amp, ph)                                 # (F, n_r, n_t, L)
-    samples = c + m + l - 1
-    iq = torch.zeros((n_pool, n_batches, n_r, samples, 2), dtype=torch.float32, device=dev)
-    for b in range(n_batches):
-        hb = h[:, :, b * nb:(b + 1) * nb, :].reshape(n_pool, n_r, -1)   # (F, n_r, nb*L)
-        body = hb @ A[:hb.shape[-1]].to(torch.complex128)               # (F, n_r, M)
-        ref = (body.abs() ** 2).mean(dim=(1, 2), keepdim=True) / (nb * l)
-        sigma = torch.sqrt(ref / (10 ** (w["snr_db"] / 10)) / 2)
-        noise = torch.complex(torch.randn(body.shape, generator=g, device=dev, dtype=torch.float64),
-                              torch.randn(body.shape, generator=g, device=dev, dtype=torch.float64))
-        body = body + sigma * noise
-        iq[:, b, :, c:c + m, 0] = body.real.float()
-        iq[:, b, :, c:c + m, 1] = body.imag.float()
-        iq[:, b, :, :c, 0] = body.real[..., m - c:].float()
-        iq[:, b, :, :c, 1] = body.imag[..., m - c:].float()
-    return iq, h.to(torch.complex64)
-
-
 def cpu_reference_rate(w, seconds, threads=None):
     """Time the oracle port of process_frames (reference64, experiments.py:176-208) on the
     host cores over a bounded sample; returns (CSI estimates/s, cores, sample description)."""
@@ -230,13 +194,23 @@ def run_gpu(args, rank, world):
     cfg = P.PilotConfig(m=w["m"], c=w["c"], n_t=w["n_t"], n_batch=w["n_batch"], l=w["l"], f_s=10e6)
     corr = P.Correlator(P.default_spec(10), cfg, w["n_r"], dtype=args.dtype, device=dev)
 
-    # --- resident synthetic input: a pool of distinct frame-sets tiled to F (> L2)
-    pool_n = min(F, 64)
-    pool, h_pool = synth_iq_pool(corr, pool_n, w, seed=1234 + rank, dev=dev)
+    # --- resident synthetic input: F distinct frame-sets synthesised on the device by the
+    # library's own channel draw + pilot sweep + AWGN (untimed input synthesis)
+    from paper_2206_05506_b200 import synth as S
+    Fq = min(F, args.scored_frames) if not args.no_quality else 0
+    ts0 = time.perf_counter()
     iq = torch.empty(corr.iq_shape(F), dtype=torch.float32, device=dev)
-    for s in range(0, F, pool_n):
-        e = min(F, s + pool_n)
-        iq[s:e].copy_(pool[:e - s])
+    h_q = None
+    chunk = 2048
+    for s0 in range(0, F, chunk):
+        e0 = min(F, s0 + chunk)
+        h = S.draw_channel(corr, e0 - s0, seed=(1234 + rank) * 1_000_003 + s0)
+        S.simulate_frames(corr, h, w["snr_db"], seed=(4321 + rank) * 1_000_003 + s0, out=iq[s0:e0])
+        if s0 < Fq:
+            h_q = h[:Fq - s0].clone() if h_q is None else torch.cat([h_q, h[:Fq - s0]])
+        del h
+    torch.cuda.synchronize(dev)
+    synth_s = time.perf_counter() - ts0
     taps = torch.empty(corr.taps_shape(F), dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
     L = _lib.lib()
@@ -291,18 +265,13 @@ def run_gpu(args, rank, world):
         except Exception:
             traffic = None
 
-    # --- estimate quality on the synthetic pool: fused scoring + NCCL all-reduce of the
+    # --- estimate quality on the synthetic input: fused scoring + NCCL all-reduce of the
     # per-rank error sums (the only collective of the path)
     from paper_2206_05506_b200 import distributed as D
     quality = None
     if not args.no_quality:
-        # fused scoring (taps + per-frame sums + per-link MSE) over Fq frame-sets of the
-        # resident input (the pool tiled) against the matching tiled truth
-        Fq = min(F, args.scored_frames)
-        h_q = torch.empty((Fq,) + tuple(h_pool.shape[1:]), dtype=h_pool.dtype, device=dev)
-        for s0 in range(0, Fq, pool_n):
-            e0 = min(Fq, s0 + pool_n)
-            h_q[s0:e0].copy_(h_pool[:e0 - s0])
+        # fused scoring (taps + per-frame sums + per-link MSE) over the first Fq frame-sets
+        # against their true channels
         q_stats = torch.zeros((Fq, 4), dtype=torch.float64, device=dev)
         q_link = torch.zeros((Fq, w["n_r"], w["n_t"]), dtype=torch.float32, device=dev)
         corr.process_scored(iq[:Fq], h_q, out=taps[:Fq], stats=q_stats, link_mse=q_link)  # warm-up
@@ -321,7 +290,6 @@ def run_gpu(args, rank, world):
         quality["scored_us_per_frame"] = q0.elapsed_time(q1) * 1e3 / Fq
         quality["scored_bytes_per_frame"] = bytes_fused_f + w["n_r"] * w["n_t"] * w["l"] * 8
         del h_q, q_stats, q_link
-    del pool
 
     # --- GEMM-only leg (K3 on the pre-packed fp16 operand): the north-star tensor-% number
     gemm = None
@@ -418,7 +386,9 @@ def run_gpu(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "us_per_frame": ms_per_step * 1e3 / F, "frames_per_s": frames_per_s,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": args.dtype, "data": "synthetic (device-generated, draw_channel law, 10 dB AWGN)",
+            "dtype": args.dtype,
+            "data": f"synthetic: {F} distinct frame-sets from the device synthesiser (draw_channel law, "
+                    f"pilot sweep, {w['snr_db']:g} dB AWGN; {synth_s:.2f} s, untimed)",
             "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8 (BASELINE configs[2])",
                        "frames_per_step": F, "input_bytes_per_step": iq.numel() * 4,
                        "l2": "inputs (47 GB f32 IQ at 10k frames) >> 126 MB L2; no flush needed",

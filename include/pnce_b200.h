@@ -130,6 +130,23 @@ pnce_status_t pnce_process_frames_scored(const pnce_plan_t* plan, const float* i
                                          const float* truth, double* stats, float* link_err,
                                          int64_t n_frames, void* stream);
 
+/* Input synthesis on the device (channel.py:96-214).  Not part of the timed
+ * estimation path: it feeds benches and sweeps with statistically equivalent frames
+ * (Philox streams instead of numpy's PCG64).
+ *
+ * pnce_draw_channel: h complex64 [F][n_r][n_t][L] with the draw_channel law
+ * (channel.py:96-108): l_nz distinct taps per link, |h| uniform on (0, A_max],
+ * A_max^2 = 1 / (n_t sqrt(l_nz)), phase uniform on [0, 2 pi).
+ *
+ * pnce_simulate_frames: the pilot sweep of simulate_frame (channel.py:186-214) for each
+ * frame-set: iq float32 [F][n_batches][n_r][P+L-1][2] = linear convolution of every
+ * batch pilot [CP | PN rolled by its shift] with its CIR, plus complex AWGN at snr_db
+ * relative to the noise_reference_power (channel.py:175-183); snr_db = +inf: noiseless. */
+pnce_status_t pnce_draw_channel(const pnce_plan_t* plan, int32_t l_nz, uint64_t seed, float* h,
+                                int64_t n_frames, void* stream);
+pnce_status_t pnce_simulate_frames(const pnce_plan_t* plan, const float* h, double snr_db,
+                                   uint64_t seed, float* iq, int64_t n_frames, void* stream);
+
 /* Launch-count accounting: number of device kernels this library has
  * launched in the calling process (for bench.py's gpu_launches). */
 int64_t pnce_kernel_launches(void);

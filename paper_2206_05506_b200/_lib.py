@@ -36,7 +36,7 @@ EXPORTS = (
     "pnce_version", "pnce_last_error", "pnce_config_check", "pnce_generate_mseq",
     "pnce_plan_create", "pnce_plan_destroy", "pnce_plan_chips", "pnce_workspace_bytes",
     "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored",
-    "pnce_kernel_launches",
+    "pnce_draw_channel", "pnce_simulate_frames", "pnce_kernel_launches",
 )
 
 
@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    u64, f64 = ctypes.c_uint64, ctypes.c_double
     cfgp = ctypes.POINTER(CfgStruct)
     sig = {
         "pnce_version": (i32, []),
@@ -78,6 +79,8 @@ def lib() -> ctypes.CDLL:
         "pnce_correlate": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames": (i32, [vp, vp, vp, vp, vp, vp, sz, i64, vp]),
         "pnce_process_frames_scored": (i32, [vp, vp, vp, vp, vp, vp, i64, vp]),
+        "pnce_draw_channel": (i32, [vp, i32, u64, vp, i64, vp]),
+        "pnce_simulate_frames": (i32, [vp, vp, f64, u64, vp, i64, vp]),
         "pnce_kernel_launches": (i64, []),
     }
     for name, (res, args) in sig.items():

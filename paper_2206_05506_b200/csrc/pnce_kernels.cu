@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "../../include/pnce_b200.h"
+#include "pnce_internal.h"
 #include "sm100_ptx.cuh"
 
 using namespace pnce;
@@ -219,8 +220,6 @@ constexpr int kWarps = 16;
 constexpr int kThreadsK3 = kWarps * 32;
 constexpr int kConvWarp0 = 4;
 constexpr int kConvWarps = 8;
-constexpr int kEpiWarp0 = 12;
-constexpr int kEpiWarps = 4;
 constexpr int kLinksPerTile = kBM / 2;                                        // 64 links per CTA
 constexpr int kRawChunk = kBK / 2;  // samples per raw staging chunk (half a K-block)
 
@@ -625,7 +624,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     constexpr bool RAW = MODE == kModeFusedTma;     // f32 rows TMA-staged, converted
     constexpr bool FLDG = MODE == kModeFusedLdg;    // f32 rows LDG'd, converted
     constexpr bool PLDG = MODE == kModePackedLdg;   // packed 16-bit rows LDG'd
-    constexpr bool FUSED = RAW || FLDG;
     // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
     // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
     constexpr int kCW = (SCORED && RAW) ? 4 : kConvWarps;
@@ -1230,6 +1228,12 @@ struct pnce_plan {
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
 };
+
+namespace pnce_internal {
+PlanView plan_view(const pnce_plan_t* p) { return PlanView{p->cfg, p->n_batches, p->chips}; }
+pnce_status_t set_error(pnce_status_t code, const std::string& msg) { return fail(code, msg); }
+void count_launch() { g_launches++; }
+}  // namespace pnce_internal
 
 static void make_tiling(Tiling& t, int r_total, int max_group) {
     const int r16 = (r_total + 15) / 16 * 16;
