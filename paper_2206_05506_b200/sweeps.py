@@ -1,0 +1,291 @@
+"""Monte-Carlo sweeps on the device, sharded over GPUs.
+
+Counterpart of the reference harness (pnce/experiments.py:45-97, 234-348) and its
+fixed-schema CSV records (pnce/records.py:15-117): the same `ExperimentConfig` grid,
+`SweepResult` rows and CSV bytes, with every sweep point computed on the GPU --
+channel draws and pilot sweeps by the device synthesiser (synth.py), estimation and
+MAE scoring by the fused correlator -- and the points of a grid distributed round-robin
+over the ranks of a process group (NCCL/gloo), gathered in grid order on rank 0.
+
+Per point and iteration the (channel, noise) seeds derive from the master seed and the
+grid key exactly as the reference does (numpy SeedSequence, experiments.py:151-154);
+they seed Philox streams, so MAE values are statistically -- not draw-for-draw --
+equivalent.  `latency_s` is the device time per frame-set of the fused scored kernel.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from .errors import InvalidConfigError, SchemaMismatchError
+
+DEFAULT_SNR_GRID_DB = tuple(float(s) for s in range(-10, 31, 5))
+
+CSV_COLUMNS = ("experiment", "backend", "nt", "nr", "m", "c", "l", "l_nz", "n_batch", "snr_db", "iterations",
+               "seed", "mae", "latency_s", "samples_moved", "macs", "saturations")
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """experiments.py:45-80 (backend = operand dtype of the device path)."""
+
+    n_t: int = 16
+    n_r: int = 16
+    pn_lengths: tuple[int, ...] = (511, 1023, 2047)
+    c: int = 64
+    l: int = 64
+    l_nz: tuple[int, ...] = (64,)
+    n_batch: tuple[int, ...] = (1,)
+    snr_db: tuple[float, ...] = DEFAULT_SNR_GRID_DB
+    iterations: int = 50
+    seed: int = 0
+    backend: str = "fp16"
+    f_s: float = 10e6
+    emit_per_iteration: bool = False
+    record_latency: bool = True
+
+    def __post_init__(self):
+        if self.iterations < 1:
+            raise InvalidConfigError("iterations must be >= 1")
+        for m in self.pn_lengths:
+            degree = (m + 1).bit_length() - 1
+            if (1 << degree) - 1 != m:
+                raise InvalidConfigError(f"PN length {m} is not 2**k - 1")
+        if not self.pn_lengths or not self.l_nz or not self.n_batch or not self.snr_db:
+            raise InvalidConfigError("grid lists must be non-empty")
+
+
+@dataclass(frozen=True)
+class SweepResult:
+    """experiments.py:83-97: one CSV row."""
+
+    experiment: str
+    backend: str
+    n_t: int
+    n_r: int
+    m: int
+    c: int
+    l: int
+    l_nz: int
+    n_batch: int
+    snr_db: float
+    iterations: int
+    seed: int
+    mae: float
+    latency_s: float
+    samples_moved: int
+    macs: int
+    saturations: int
+
+
+def derive_seeds(master: int, *key: int) -> tuple[int, int]:
+    """experiments.py:151-154: (channel seed, noise seed) from SeedSequence([master, *key])."""
+    chan, noise = np.random.SeedSequence([master, *key]).generate_state(2, dtype=np.uint64)
+    return int(chan), int(noise)
+
+
+# ---------------------------------------------------------------- records (records.py)
+def _fmt(x: float) -> str:
+    return f"{x:.9g}"
+
+
+def render_row(r: SweepResult) -> str:
+    return ",".join([r.experiment, r.backend, str(r.n_t), str(r.n_r), str(r.m), str(r.c), str(r.l), str(r.l_nz),
+                     str(r.n_batch), _fmt(r.snr_db), str(r.iterations), str(r.seed), _fmt(r.mae),
+                     _fmt(r.latency_s), str(r.samples_moved), str(r.macs), str(r.saturations)])
+
+
+def render_csv(rows: Iterable[SweepResult]) -> str:
+    return "\n".join([",".join(CSV_COLUMNS), *(render_row(r) for r in rows)]) + "\n"
+
+
+def parse_csv(text: str) -> list[SweepResult]:
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines:
+        raise SchemaMismatchError("empty CSV: header row missing")
+    header = tuple(lines[0].split(","))
+    if header != CSV_COLUMNS:
+        raise SchemaMismatchError(f"header {header} != expected {CSV_COLUMNS}")
+    out = []
+    for ln in lines[1:]:
+        p = ln.split(",")
+        if len(p) != len(CSV_COLUMNS):
+            raise SchemaMismatchError(f"row has {len(p)} fields, expected {len(CSV_COLUMNS)}")
+        out.append(SweepResult(p[0], p[1], int(p[2]), int(p[3]), int(p[4]), int(p[5]), int(p[6]), int(p[7]),
+                               int(p[8]), float(p[9]), int(p[10]), int(p[11]), float(p[12]), float(p[13]),
+                               int(p[14]), int(p[15]), int(p[16])))
+    return out
+
+
+def write_csv(path, rows: Sequence[SweepResult]) -> None:
+    with open(path, "w", newline="") as fh:
+        fh.write(render_csv(rows))
+
+
+def read_csv(path) -> list[SweepResult]:
+    with open(path) as fh:
+        return parse_csv(fh.read())
+
+
+# ---------------------------------------------------------------- grid + sharding
+@dataclass(frozen=True)
+class SweepPoint:
+    experiment: str
+    m: int
+    n_batch: int
+    l_nz: int
+    snr_db: float
+    si: int
+
+
+def snr_sweep_points(cfg: ExperimentConfig) -> list[SweepPoint]:
+    """run_snr_sweep (experiments.py:299-322) grid order."""
+    return [SweepPoint("snr_sweep", m, nb, cfg.l_nz[0], snr, si)
+            for m in cfg.pn_lengths for nb in cfg.n_batch for si, snr in enumerate(cfg.snr_db)]
+
+
+def tap_sweep_points(cfg: ExperimentConfig) -> list[SweepPoint]:
+    """run_tap_sweep (experiments.py:325-348) grid order."""
+    m, nb = cfg.pn_lengths[0], cfg.n_batch[0]
+    return [SweepPoint("tap_sweep", m, nb, lnz, snr, si) for lnz in cfg.l_nz for si, snr in enumerate(cfg.snr_db)]
+
+
+def shard(points: Sequence, rank: int, world: int) -> list[tuple[int, object]]:
+    """Round-robin (index, point) assignment: neighbouring grid points (similar cost) spread."""
+    return [(i, p) for i, p in enumerate(points) if i % world == rank]
+
+
+def _gather_rows(indexed_rows: list[tuple[int, list[SweepResult]]], group=None) -> list[SweepResult] | None:
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return [r for _, rows in sorted(indexed_rows, key=lambda x: x[0]) for r in rows]
+    world = dist.get_world_size(group)
+    parts = [None] * world if dist.get_rank(group) == 0 else None
+    dist.gather_object(indexed_rows, parts, dst=0, group=group)
+    if dist.get_rank(group) != 0:
+        return None
+    merged = [x for part in parts for x in part]
+    return [r for _, rows in sorted(merged, key=lambda x: x[0]) for r in rows]
+
+
+# ---------------------------------------------------------------- device evaluation
+_CORR_CACHE: dict = {}
+
+
+def _correlator(cfg: ExperimentConfig, m: int, n_batch: int, device: torch.device):
+    from .estimator import Correlator
+    from .pilots import PilotConfig
+    from .pn import default_spec
+    key = (m, n_batch, cfg.n_t, cfg.n_r, cfg.c, cfg.l, cfg.backend, str(device))
+    if key not in _CORR_CACHE:
+        pilot = PilotConfig(m=m, c=cfg.c, n_t=cfg.n_t, n_batch=n_batch, l=cfg.l, f_s=cfg.f_s)
+        _CORR_CACHE[key] = Correlator(default_spec((m + 1).bit_length() - 1), pilot, cfg.n_r,
+                                      dtype=cfg.backend, device=device)
+    return _CORR_CACHE[key]
+
+
+def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device) -> list[SweepResult]:
+    """_sweep_point (experiments.py:234-296) on the device: all iterations as one batch."""
+    from . import synth
+    corr = _correlator(cfg, pt.m, pt.n_batch, device)
+    it_n = cfg.iterations
+    seeds = [derive_seeds(cfg.seed, pt.m, pt.n_batch, pt.l_nz, pt.si, it) for it in range(it_n)]
+    h = torch.empty(corr.taps_shape(it_n), dtype=torch.complex64, device=device)
+    iq = torch.empty(corr.iq_shape(it_n), dtype=torch.float32, device=device)
+    for it, (cs, ns) in enumerate(seeds):
+        h[it:it + 1] = synth.draw_channel(corr, 1, l_nz=pt.l_nz, seed=cs)
+        synth.simulate_frames(corr, h[it:it + 1], pt.snr_db, seed=ns, out=iq[it:it + 1])
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    _, stats, _ = corr.process_scored(iq, h)
+    ev1.record()
+    torch.cuda.synchronize(device)
+    per_frame = (ev0.elapsed_time(ev1) / 1e3) / it_n if cfg.record_latency else 0.0
+    n_taps = cfg.n_r * cfg.n_t * cfg.l
+    maes = (stats[:, 0] / n_taps).tolist()
+    sats = stats[:, 2].round().long().tolist()
+    pil = corr.cfg
+    samples_moved = pil.n_batches * cfg.n_r * pil.p
+    macs = cfg.n_t * cfg.l * pt.m * cfg.n_r
+    backend = f"tcgen05-{cfg.backend}"
+
+    def row(name, iters, seed, mae_v, lat, sat):
+        return SweepResult(name, backend, cfg.n_t, cfg.n_r, pt.m, cfg.c, cfg.l, pt.l_nz, pt.n_batch, pt.snr_db,
+                           iters, seed, mae_v, lat, samples_moved, macs, sat)
+
+    rows = [row(pt.experiment, it_n, cfg.seed, math.fsum(maes) / it_n, per_frame, int(sum(sats)))]
+    if cfg.emit_per_iteration:
+        rows += [row(f"{pt.experiment}:iter", 1, seeds[it][0], maes[it], per_frame, sats[it]) for it in range(it_n)]
+    return rows
+
+
+def _run(cfg: ExperimentConfig, points: Sequence[SweepPoint], device=None, group=None) -> list[SweepResult] | None:
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    if device is None:
+        device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
+    mine = [(i, evaluate_point(cfg, pt, device)) for i, pt in shard(points, rank, world)]
+    return _gather_rows(mine, group)
+
+
+def run_snr_sweep(cfg: ExperimentConfig, device=None, group=None) -> list[SweepResult] | None:
+    """MAE vs SNR over the (PN length, N_batch) grid; rows on rank 0 (None elsewhere)."""
+    return _run(cfg, snr_sweep_points(cfg), device, group)
+
+
+def run_tap_sweep(cfg: ExperimentConfig, device=None, group=None) -> list[SweepResult] | None:
+    """MAE vs SNR while varying the tap count (M, N_batch fixed to the grid heads)."""
+    return _run(cfg, tap_sweep_points(cfg), device, group)
+
+
+def main(argv=None) -> int:
+    """`python -m paper_2206_05506_b200.sweeps` (torchrun for several GPUs): the reference CLI's
+    `snr-sweep` / `tap-sweep` on the device, CSV on rank 0."""
+    import argparse
+
+    import torch.distributed as dist
+    ap = argparse.ArgumentParser(description=main.__doc__)
+    ap.add_argument("experiment", choices=["snr", "tap"])
+    ap.add_argument("--out", default="-")
+    ap.add_argument("--nt", type=int, default=16)
+    ap.add_argument("--nr", type=int, default=16)
+    ap.add_argument("--m", type=int, nargs="+", default=[511, 1023, 2047])
+    ap.add_argument("--c", type=int, default=64)
+    ap.add_argument("--l", type=int, default=64)
+    ap.add_argument("--l-nz", type=int, nargs="+", default=None)
+    ap.add_argument("--n-batch", type=int, nargs="+", default=[1])
+    ap.add_argument("--snr", type=float, nargs="+", default=list(DEFAULT_SNR_GRID_DB))
+    ap.add_argument("--iterations", type=int, default=50)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--per-iteration", action="store_true")
+    a = ap.parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    cfg = ExperimentConfig(n_t=a.nt, n_r=a.nr, pn_lengths=tuple(a.m), c=a.c, l=a.l,
+                           l_nz=tuple(a.l_nz or [a.l]), n_batch=tuple(a.n_batch), snr_db=tuple(a.snr),
+                           iterations=a.iterations, seed=a.seed, backend=a.dtype, emit_per_iteration=a.per_iteration)
+    rows = (run_snr_sweep if a.experiment == "snr" else run_tap_sweep)(cfg)
+    if rows is not None:
+        text = render_csv(rows)
+        if a.out == "-":
+            print(text, end="")
+        else:
+            with open(a.out, "w", newline="") as fh:
+                fh.write(text)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -1,0 +1,60 @@
+"""Device sweeps against the reference's own sweep output."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2206_05506_b200 import sweeps as SW
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def test_snr_sweep_rows_match_reference_csv(dev):
+    """Same grid, schema, seeds and counters as the reference's run_snr_sweep (4x4, M 63/127);
+    MAE statistically equal (4 iterations per point on each side)."""
+    with open(os.path.join(GOLD, "ref_snr_sweep.csv"), newline="") as fh:
+        ref = SW.parse_csv(fh.read())
+    cfg = SW.ExperimentConfig(n_t=4, n_r=4, pn_lengths=(63, 127), c=16, l=16, l_nz=(16,), n_batch=(1,),
+                              snr_db=(-10.0, 10.0, 30.0), iterations=4, seed=0, record_latency=False)
+    rows = SW.run_snr_sweep(cfg, device=dev)
+    assert len(rows) == len(ref)
+    for a, b in zip(rows, ref):
+        assert (a.experiment, a.n_t, a.n_r, a.m, a.c, a.l, a.l_nz, a.n_batch, a.snr_db, a.iterations, a.seed,
+                a.samples_moved, a.macs, a.saturations) == \
+               (b.experiment, b.n_t, b.n_r, b.m, b.c, b.l, b.l_nz, b.n_batch, b.snr_db, b.iterations, b.seed,
+                b.samples_moved, b.macs, b.saturations)
+        assert a.backend == "tcgen05-fp16" and a.latency_s == 0.0
+        assert abs(math.log(a.mae / b.mae)) < 0.25, (a, b)
+    text = SW.render_csv(rows)                      # 9-digit rendering: stable after one round trip
+    assert SW.render_csv(SW.parse_csv(text)) == text
+
+
+def test_cfg2_mae_curve(dev):
+    """cfg2 (16x16, M=255, L=C=32, N_b=4) MAE vs SNR with 64 iterations per point against
+    the reference64 anchor (8 frame-sets per point): within 8 %."""
+    gold = np.load(os.path.join(GOLD, "golden.npz"))
+    snrs, mae_ref = gold["curve_snr"], gold["curve_mae32"].mean(axis=1)
+    cfg = SW.ExperimentConfig(n_t=16, n_r=16, pn_lengths=(255,), c=32, l=32, l_nz=(32,), n_batch=(4,),
+                              snr_db=tuple(float(s) for s in snrs), iterations=64, seed=0, emit_per_iteration=True)
+    rows = SW.run_snr_sweep(cfg, device=dev)
+    head = [r for r in rows if r.experiment == "snr_sweep"]
+    per_it = [r for r in rows if r.experiment == "snr_sweep:iter"]
+    assert len(head) == len(snrs) and len(per_it) == 64 * len(snrs)
+    for r, want in zip(head, mae_ref):
+        assert abs(r.mae / want - 1) < 0.08, (r.snr_db, r.mae, want)
+        assert r.latency_s > 0
+    # the head row is the mean of its per-iteration rows
+    for k, r in enumerate(head):
+        its = per_it[64 * k:64 * (k + 1)]
+        assert math.isclose(r.mae, math.fsum(x.mae for x in its) / 64, rel_tol=1e-12)
