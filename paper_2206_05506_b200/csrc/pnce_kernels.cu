@@ -616,7 +616,7 @@ __device__ __forceinline__ void prefetch_raw_chunk(const CorrParams& p, const CU
     tma_prefetch_l2_2d(tm, (2 * (p.c + kb * kBK + (jc & 1) * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile);
 }
 
-template <int MODE, bool SCORED>
+template <int MODE, bool SCORED, bool EPI8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
@@ -626,7 +626,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     constexpr bool PLDG = MODE == kModePackedLdg;   // packed 16-bit rows LDG'd
     // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
     // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
-    constexpr int kCW = (SCORED && RAW) ? 4 : kConvWarps;
+    // (packed/TMA mode has no converter work: EPI8 moves 4 of those warps to the epilogue)
+    constexpr int kCW = ((SCORED || EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
     constexpr int kEW0 = kConvWarp0 + kCW;
     constexpr int kEW = kWarps - kEW0;
     // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
@@ -1261,6 +1262,9 @@ static cudaError_t set_smem_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_correlate<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_correlate<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
+        e = cudaFuncSetAttribute(k_correlate<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemLimit);
     return e;
 }
 
@@ -1269,8 +1273,17 @@ static cudaError_t set_smem_attrs() {
 template <int MODE>
 static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
                       const CUtensorMap& b, const CorrParams& prm) {
+    // 8 epilogue warps: +1 % for the packed operand (its converter warps are idle anyway),
+    // -5 % for the fused path (converters become the bottleneck); PNCE_TUNE_EPI8 overrides
+    static const int epi8_env = [] {
+        const char* e = std::getenv("PNCE_TUNE_EPI8");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
     if (scored)
         k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+    else if ((MODE == kModeFusedTma || MODE == kModePacked) && epi8)
+        k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
     else
         k_correlate<MODE, false><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
 }
