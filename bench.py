@@ -291,6 +291,24 @@ def run_gpu(args, rank, world):
         quality["scored_bytes_per_frame"] = bytes_fused_f + w["n_r"] * w["n_t"] * w["l"] * 8
         del h_q, q_stats, q_link
 
+    # --- tensor16 leg: the reference's tensor16 backend on the tensor cores,
+    # binary16 partials per 256-sample chunk folded into an fp32 total in TMEM
+    t16 = None
+    if not args.no_quality:
+        Ft = min(F, args.scored_frames)
+        st16 = torch.zeros((Ft, 4), dtype=torch.float64, device=dev)
+        corr.process_tensor16(iq[:Ft], chunk_len=256, accumulator="binary16", out=taps[:Ft], stats=st16)
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st16.zero_()
+        t0e.record()
+        corr.process_tensor16(iq[:Ft], chunk_len=256, accumulator="binary16", out=taps[:Ft], stats=st16)
+        t1e.record()
+        torch.cuda.synchronize(dev)
+        t16 = {"chunk_len": 256, "accumulator": "binary16", "frames": Ft,
+               "us_per_frame": t0e.elapsed_time(t1e) * 1e3 / Ft,
+               "saturations": int(st16[:, 3].sum().item()), "nonfinite": int(st16[:, 2].sum().item())}
+        del st16
+
     # --- GEMM-only leg (K3 on the pre-packed fp16 operand): the north-star tensor-% number
     gemm = None
     if not args.no_gemm_leg:
@@ -404,6 +422,7 @@ def run_gpu(args, rank, world):
                                          "frames_per_launch": F}},
             "gemm_leg": gemm,
             "estimate_quality": quality,
+            "tensor16_leg": t16,
             "cpu_baseline": cpu, "e2e": e2e, "ingest_iq_file": ingest, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

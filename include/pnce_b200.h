@@ -130,6 +130,20 @@ pnce_status_t pnce_process_frames_scored(const pnce_plan_t* plan, const float* i
                                          const float* truth, double* stats, float* link_err,
                                          int64_t n_frames, void* stream);
 
+/* The reference's tensor16 backend on real tensor cores (halfprec.py:93-125):
+ * fp16/bf16 operands, the contraction split into chunk_len-sample chunks (0: one chunk;
+ * otherwise a multiple of 64 and <= roundup(m, 4)), each chunk accumulated in TMEM as a
+ * binary32 (binary16_accumulator = 0) or binary16 (= 1, the F16 tcgen05 accumulator)
+ * partial, then x fp32(1/M) into an fp32 running total.  A (frame-set, batch) whose partial
+ * or total goes non-finite is scored as all-zero taps and counted, as process_frames
+ * does (experiments.py:201-205).  stats (nullable, zeroed by the caller) [F][4]:
+ * sum|e|, sum|e|^2 (when truth != NULL), non-finite taps, saturations (n_r * n_tx per
+ * saturated batch, the reference's unit). */
+pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* plan, const float* iq, float* taps,
+                                           const float* truth, double* stats, int32_t chunk_len,
+                                           int32_t binary16_accumulator, int64_t n_frames,
+                                           void* stream);
+
 /* Input synthesis on the device (channel.py:96-214).  Not part of the timed
  * estimation path: it feeds benches and sweeps with statistically equivalent frames
  * (Philox streams instead of numpy's PCG64).

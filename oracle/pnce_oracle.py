@@ -215,7 +215,7 @@ def mma_correlate(a: np.ndarray, y: np.ndarray, norm_len: int, chunk_len=256,
 
 
 def correlate_rows(rows: np.ndarray, y: np.ndarray, backend: str, norm_len: int,
-                   chunk_len=256) -> np.ndarray:
+                   chunk_len=256, accumulator: str = "binary32") -> np.ndarray:
     """estimator.py:68-86 dispatch (reference64 / reference32 / tensor16)."""
     if backend == "reference64":
         re = rows @ np.ascontiguousarray(y.real)
@@ -227,12 +227,12 @@ def correlate_rows(rows: np.ndarray, y: np.ndarray, backend: str, norm_len: int,
         im = r32 @ y.imag.astype(np.float32) / np.float32(norm_len)
         return re.astype(np.float64) + 1j * im.astype(np.float64)
     if backend == "tensor16":
-        return mma_correlate(rows, y, norm_len, chunk_len=chunk_len)
+        return mma_correlate(rows, y, norm_len, chunk_len=chunk_len, accumulator=accumulator)
     raise OracleError(f"unknown backend {backend!r}")
 
 
 def process_frames(chips: np.ndarray, cfg: Config, frames, backend: str = "reference64",
-                   rows_per_batch=None, chunk_len=256):
+                   rows_per_batch=None, chunk_len=256, accumulator: str = "binary32"):
     """experiments.py:176-208: CP strip, correlate, demux into taps[r, t, l].
 
     ``frames`` is a sequence of (n_r, P + L - 1) complex arrays, one per batch.
@@ -249,7 +249,7 @@ def process_frames(chips: np.ndarray, cfg: Config, frames, backend: str = "refer
         body = np.ascontiguousarray(remove_cp(frame, cfg.c, cfg.m).T)
         macs += rows.shape[0] * cfg.m * n_r
         try:
-            flat = correlate_rows(rows, body, backend, cfg.m, chunk_len)
+            flat = correlate_rows(rows, body, backend, cfg.m, chunk_len, accumulator)
         except FloatingPointError:
             saturations += n_r * len(batch)
             continue

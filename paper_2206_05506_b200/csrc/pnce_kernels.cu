@@ -258,6 +258,11 @@ struct CorrParams {
     double* stats;
     float* link_err;  // optional [F][n_r][n_t]: mean_l |h_est - h_true|^2 per link (needs truth)
     float inv_l;
+    // tensor16 emulation on real tensor cores (halfprec.py:93-125): accumulation units of
+    // chunk_kb K-blocks, each folded x fp32(1/M) into an fp32 running total kept in TMEM
+    int32_t chunk_kb;    // K-blocks per accumulation unit (= k_blocks outside tensor16 mode)
+    int32_t acc16;       // 1: binary16 partials (F16 TMEM accumulator), 0: binary32
+    uint32_t* sat_flags; // tensor16: [F][n_batches] set when a partial / total is non-finite
 };
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
@@ -616,7 +621,58 @@ __device__ __forceinline__ void prefetch_raw_chunk(const CorrParams& p, const CU
     tma_prefetch_l2_2d(tm, (2 * (p.c + kb * kBK + (jc & 1) * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile);
 }
 
-template <int MODE, bool SCORED, bool EPI8 = false>
+// tensor16 fold (halfprec.py:104-125 on real tensor cores): the accumulation unit just
+// finished in TMEM (binary16 or binary32 partial of one chunk) is widened to fp32, scaled
+// by fp32(1/M) and added to the fp32 running total in TMEM (two roundings, as the
+// reference's `total + acc * scale`); the last unit writes the demuxed taps.  Any
+// non-finite partial or total raises the (frame-set, batch) saturation flag.
+__device__ __forceinline__ void t16_fold(const CorrParams& p, uint32_t t_part, uint32_t t_tot, const EpiLink& e,
+                                         int n0, bool first, bool last, bool& sat) {
+    for (int c = 0; c < p.g_cols; c += 32) {
+        uint32_t d[16], t[16];
+        tmem_ld_16x256b_x4(t_part + c, d);
+        if (!first) tmem_ld_16x256b_x4(t_tot + c, t);
+        tmem_wait_ld();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float x = p.acc16 ? __half2float(__ushort_as_half((unsigned short)(d[i] & 0xffffu)))
+                                    : __uint_as_float(d[i]);
+            if (!isfinite(x)) sat = true;
+            const float y = __fmul_rn(x, p.inv_m);
+            v[i] = first ? y : __fadd_rn(__uint_as_float(t[i]), y);
+        }
+        if (!last) {
+            uint32_t w[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(v[i]);
+            tmem_st_16x256b_x4(t_tot + c, w);
+        } else if (e.out >= 0) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int lag = n0 + c + 8 * r;
+                const float re0 = v[4 * r], re1 = v[4 * r + 1], im0 = v[4 * r + 2], im1 = v[4 * r + 3];
+                if (lag >= e.n_valid) continue;
+                if (!(isfinite(re0) && isfinite(im0))) sat = true;
+                float* dst = p.taps + 2 * (e.out + lag);
+                if (lag + 1 < e.n_valid) {
+                    if (!(isfinite(re1) && isfinite(im1))) sat = true;
+                    if (e.vec) {
+                        st_global_v4(dst, re0, im0, re1, im1);
+                    } else {
+                        *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+                        *reinterpret_cast<float2*>(dst + 2) = make_float2(re1, im1);
+                    }
+                } else {
+                    *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+                }
+            }
+        }
+    }
+    if (!last) tmem_wait_st();
+}
+
+template <int MODE, bool SCORED, bool EPI8 = false, bool T16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const CorrParams p) {
@@ -744,13 +800,17 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #endif
             PROF_BEGIN(3);
             for (int ti = 0; ti < my_tiles; ++ti) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                PROF_MARK(0);
-                TRACE(1, ti);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
+                uint32_t d_tmem = 0;
+                int kc = 0;  // K-block within the accumulation unit (the whole K outside tensor16)
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     const int j = ti * p.k_blocks + kb;
+                    if (kc == 0) {
+                        mbar_wait(&tempty[acc], acc_phase ^ 1);
+                        PROF_MARK(0);
+                        TRACE(1, ti);
+                        tc_fence_after();
+                        d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
+                    }
 #ifndef PNCE_DIAG_NO_FULLWAIT
                     mbar_wait(&full[stage], phase);
 #else
@@ -766,7 +826,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
                         for (int jj = 0; jj < p.n_mma; ++jj) {
                             const uint64_t bd = make_sdesc(sb + jj * b_half_bytes + ks * 32, 16, 1024, 2);
-                            umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
+                            umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kc | ks) != 0);
                         }
                     }
                     umma_commit_pair(&empty[stage]);
@@ -774,9 +834,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     (void)j;
                     if (++stage == S) { stage = 0; phase ^= 1u; }
                     PROF_MARK(2);
+                    if (++kc == p.chunk_kb || kb == p.k_blocks - 1) {
+                        umma_commit_pair(&tfull[acc]);
+                        if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
+                        kc = 0;
+                    }
                 }
-                umma_commit_pair(&tfull[acc]);
-                if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
             PROF_END(2, 3);
 #ifdef PNCE_DIAG_PROF
@@ -1033,6 +1096,40 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         int acc = 0;
         uint32_t acc_phase = 0;
         PROF_BEGIN(2);
+        if constexpr (T16) {
+            // accumulation units of chunk_kb K-blocks; partial at columns [0, G), running
+            // total at [G, 2G) (single-buffered: the MMA waits for each fold)
+            const int n_units = (p.k_blocks + p.chunk_kb - 1) / p.chunk_kb;
+            for (int ti = 0; ti < my_tiles; ++ti) {
+                const int tile = cid + ti * n_clusters;
+                const int mt = tile / p.n_groups;
+                const int g = tile - mt * p.n_groups;
+                const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
+                const int n0 = g * p.g_cols + colp;
+                bool sat[2] = {false, false};
+                for (int u = 0; u < n_units; ++u) {
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int k = 0; k < kBlocksPerWarp; ++k) {
+                        const int bb = bb0 + k;
+                        const EpiLink e = make_link(p, link0 + 8 * bb);
+                        const uint32_t lanes = (uint32_t)(quarter * 32 + 16 * bb) << 16;
+                        t16_fold(p, tmem_base + lanes, tmem_base + lanes + (uint32_t)p.g_cols, e, n0, u == 0,
+                                 u == n_units - 1, sat[k]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
+                    if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
+                }
+#pragma unroll
+                for (int k = 0; k < kBlocksPerWarp; ++k) {
+                    const int64_t link = link0 + 8 * (bb0 + k);
+                    if (sat[k] && link < p.total_links) atomicOr(p.sat_flags + (uint32_t)link / (uint32_t)p.n_r, 1u);
+                }
+            }
+        } else
         for (int ti = 0; ti < my_tiles; ++ti) {
             const int tile = cid + ti * n_clusters;
             const int mt = tile / p.n_groups;
@@ -1149,6 +1246,51 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     }
 }
 
+// tensor16 finish (experiments.py:201-205): a (frame-set, batch) whose partial or total
+// went non-finite is scored as all-zero taps and counted as n_r * n_tx saturations
+// (stats[:, 3]); then the per-frame error sums against the truth (stats[:, 0..2]).
+__global__ void k_t16_finish(float* __restrict__ taps, const float* __restrict__ truth, double* __restrict__ stats,
+                             const uint32_t* __restrict__ flags, int n_r, int n_t, int n_batch, int n_batches, int l) {
+    const int64_t fb = blockIdx.x;
+    const int b = (int)(fb % n_batches);
+    const int64_t f = fb / n_batches;
+    const int n_tx = min(n_batch, n_t - b * n_batch);
+    const bool sat = flags[fb] != 0;
+    const int per_r = n_tx * l;
+    float s_abs = 0.f, s_sq = 0.f, bad = 0.f;
+    for (int idx = threadIdx.x; idx < n_r * per_r; idx += blockDim.x) {
+        const int r = idx / per_r, q = idx - r * per_r;
+        const int64_t pos = ((f * n_r + r) * n_t + (int64_t)b * n_batch) * l + q;
+        float2* tp = reinterpret_cast<float2*>(taps) + pos;
+        float2 v = *tp;
+        if (sat) {
+            v = make_float2(0.f, 0.f);
+            *tp = v;
+        }
+        if (!(isfinite(v.x) && isfinite(v.y))) bad += 1.f;
+        if (truth != nullptr) {
+            const float2 h = reinterpret_cast<const float2*>(truth)[pos];
+            const float dx = v.x - h.x, dy = v.y - h.y;
+            s_sq += dx * dx + dy * dy;
+            s_abs += sqrtf(dx * dx + dy * dy);
+        }
+    }
+    if (stats == nullptr) return;
+    for (int o = 16; o > 0; o >>= 1) {
+        s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+        s_sq += __shfl_xor_sync(0xffffffffu, s_sq, o);
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (truth != nullptr) {
+            atomicAdd(&stats[f * 4 + 0], (double)s_abs);
+            atomicAdd(&stats[f * 4 + 1], (double)s_sq);
+        }
+        if (bad != 0.f) atomicAdd(&stats[f * 4 + 2], (double)bad);
+    }
+    if (threadIdx.x == 0 && sat) atomicAdd(&stats[f * 4 + 3], (double)n_r * n_tx);
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1226,6 +1368,7 @@ struct pnce_plan {
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
     Tiling packed;   // packed operand via TMA: same grouping (TMA ingress, not the drain, bounds G=256)
     Tiling packed_ldg;  // packed operand via LDG: <= 256 columns, double-buffered accumulator
+    Tiling t16;      // tensor16 emulation: <= 256 columns (multiple of 32), partial + running total
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
 };
@@ -1236,10 +1379,10 @@ pnce_status_t set_error(pnce_status_t code, const std::string& msg) { return fai
 void count_launch() { g_launches++; }
 }  // namespace pnce_internal
 
-static void make_tiling(Tiling& t, int r_total, int max_group) {
-    const int r16 = (r_total + 15) / 16 * 16;
+static void make_tiling(Tiling& t, int r_total, int max_group, int align = 16) {
+    const int r16 = (r_total + align - 1) / align * align;
     t.n_groups = (r16 + max_group - 1) / max_group;
-    int g = ((r16 + t.n_groups - 1) / t.n_groups + 15) / 16 * 16;
+    int g = ((r16 + t.n_groups - 1) / t.n_groups + align - 1) / align * align;
     if (g > 256) {
         g = (g + 31) / 32 * 32;
         t.n_mma = 2;
@@ -1265,6 +1408,9 @@ static cudaError_t set_smem_attrs() {
     if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
         e = cudaFuncSetAttribute(k_correlate<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemLimit);
+    if (e == cudaSuccess && MODE == kModeFusedTma)
+        e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     return e;
 }
 
@@ -1373,8 +1519,11 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
     const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
     make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
+    make_tiling(p->t16, p->r_total, 256, 32);  // 32-column fold chunks
+    p->t16.acc_stages = 1;
+    p->t16.tmem_cols = 512;
     p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
-                              p->packed_ldg.n_groups * p->packed_ldg.g_cols});
+                              p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols});
     p->num_sms = sms;
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1412,6 +1561,8 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     if (s == PNCE_OK)
         s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
                       cfg->dtype == PNCE_DTYPE_BF16);
+    if (s == PNCE_OK)
+        s = make_tmap(&p->t16.tm_circ, p->circ, p->k_pad, circ_rows, p->t16.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
     if (s == PNCE_OK)
         s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2,
                       cfg->dtype == PNCE_DTYPE_BF16);
@@ -1552,6 +1703,7 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.inv_m = 1.0f / (float)c.m;
     prm.inv_l = 1.0f / (float)c.l;
     prm.k_pad = p->k_pad;
+    prm.chunk_kb = prm.k_blocks;
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
@@ -1603,8 +1755,13 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     return PNCE_OK;
 }
 
+struct T16Opts {
+    int chunk_kb;
+    int acc16;
+};
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
-                                         double* stats, float* link_err, int64_t n_frames, void* stream);
+                                         double* stats, float* link_err, int64_t n_frames, void* stream,
+                                         const T16Opts* t16 = nullptr);
 
 pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                   double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
@@ -1621,27 +1778,46 @@ pnce_status_t pnce_process_frames_scored(const pnce_plan_t* p, const float* iq, 
     return process_frames_impl(p, iq, taps, truth, stats, link_err, n_frames, stream);
 }
 
+pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                           double* stats, int32_t chunk_len, int32_t binary16_accumulator,
+                                           int64_t n_frames, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    const int kp4 = (p->cfg.m + 3) / 4 * 4;  // the reference pads K to its 4-wide tile (halfprec.py:80-81)
+    if (chunk_len < 0) return fail(PNCE_ERR_INVALID_CONFIG, "chunk_len must be >= 0 (0: one chunk)");
+    if (chunk_len > kp4) return fail(PNCE_ERR_INVALID_CONFIG, "chunk_len exceeds padded length");
+    if (chunk_len % kBK) return fail(PNCE_ERR_INVALID_CONFIG, "device chunks are whole 64-sample K-blocks");
+    if (binary16_accumulator != 0 && binary16_accumulator != 1)
+        return fail(PNCE_ERR_INVALID_CONFIG, "accumulator must be 0 (binary32) or 1 (binary16)");
+    T16Opts o{chunk_len ? chunk_len / kBK : p->k_pad / kBK, binary16_accumulator};
+    return process_frames_impl(p, iq, taps, truth, stats, nullptr, n_frames, stream, &o);
+}
+
 }  // extern "C"
 
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
-                                         double* stats, float* link_err, int64_t n_frames, void* stream) {
+                                         double* stats, float* link_err, int64_t n_frames, void* stream,
+                                         const T16Opts* t16) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
     CorrParams prm;
-    pnce_status_t s = fill_params(p, p->fused, true, taps, truth, stats, n_frames, prm);
+    // tensor16: scoring moves to the finish kernel (saturated batches are scored as zeros)
+    pnce_status_t s = fill_params(p, t16 ? p->t16 : p->fused, true, taps, t16 ? nullptr : truth,
+                                  t16 ? nullptr : stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
     prm.link_err = link_err;
-    const bool scored = truth || stats || link_err;
+    const bool scored = !t16 && (truth || stats || link_err);
     const int samples = prm.samples;
     const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
     // the raw f32 rows can be described by a tensor map when the row stride is 16-byte aligned
     const bool map_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
     bool use_tma = map_ok;
     if (fm && std::atoi(fm) == kModeFusedLdg) use_tma = false;
+    if (t16 && !map_ok)
+        return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     prm.raw_row_floats = 2 * kRawChunk + ((c_odd(p)) ? 4 : 0);
     CUtensorMap tm_raw;
@@ -1667,7 +1843,28 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         prm.raw_stages = raw;
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
                             (size_t)prm.raw_stages * prm.raw_stage_bytes;
-        launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, p->fused.tm_circ, prm);
+        if (t16) {
+            const int64_t n_fb = n_frames * p->n_batches;
+            uint32_t* flags = nullptr;
+            cudaError_t e = cudaMallocAsync(&flags, sizeof(uint32_t) * n_fb, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(uint32_t) * n_fb, st);
+            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16 flags: ") + cudaGetErrorString(e));
+            prm.chunk_kb = t16->chunk_kb;
+            prm.acc16 = t16->acc16;
+            prm.sat_flags = flags;
+            if (t16->acc16) prm.idesc &= ~(3u << 4);  // c_format = F16: binary16 partials in TMEM
+            k_correlate<kModeFusedTma, false, false, true><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(
+                tm_raw, p->t16.tm_circ, prm);
+            g_launches++;
+            const pnce_cfg_t& c = p->cfg;
+            k_t16_finish<<<(unsigned)n_fb, 256, 0, st>>>(taps, truth, stats, flags, c.n_r, c.n_t, c.n_batch,
+                                                         p->n_batches, c.l);
+            e = cudaGetLastError();
+            cudaFreeAsync(flags, st);
+            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16: ") + cudaGetErrorString(e));
+        } else {
+            launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, p->fused.tm_circ, prm);
+        }
     } else {
         if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;

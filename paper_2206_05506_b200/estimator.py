@@ -217,6 +217,37 @@ class Correlator:
                 ctypes.c_void_p(link_mse.data_ptr()), n_frames, _stream_ptr(self.device)))
         return out, stats, link_mse
 
+    def process_tensor16(self, iq: torch.Tensor, chunk_len: int | None = 256, accumulator: str = "binary32",
+                         truth: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                         stats: torch.Tensor | None = None):
+        """The reference's tensor16 backend (halfprec.py:93-125, `BackendConfig(kind="tensor16",
+        chunk_len, accumulator)`) on the tensor cores: chunked binary16/binary32 partials, each
+        x fp32(1/M) into an fp32 total; saturated batches scored as zeros and counted.
+        Returns (taps, stats (F, 4) f64: sum|e|, sum|e|^2, non-finite, saturations)."""
+        if accumulator not in ("binary32", "binary16"):
+            raise InvalidConfigError(f"unknown accumulator {accumulator!r}")
+        iq, n_frames = self._check_iq(iq)
+        if out is None:
+            out = torch.empty(self.taps_shape(n_frames), dtype=torch.complex64, device=self.device)
+        elif tuple(out.shape) != self.taps_shape(n_frames) or out.dtype != torch.complex64 or not out.is_contiguous():
+            raise DimensionMismatchError("out must be contiguous complex64 (F, n_r, n_t, L)")
+        truth_ptr = None
+        if truth is not None:
+            if tuple(truth.shape) != self.taps_shape(n_frames) or truth.dtype != torch.complex64 or not truth.is_cuda:
+                raise DimensionMismatchError("truth must be CUDA complex64 (F, n_r, n_t, L)")
+            truth = truth.contiguous()
+            truth_ptr = ctypes.c_void_p(truth.data_ptr())
+        if stats is None:
+            stats = torch.zeros((n_frames, 4), dtype=torch.float64, device=self.device)
+        elif tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64:
+            raise DimensionMismatchError("stats must be float64 (F, 4)")
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().pnce_process_frames_tensor16(
+                self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()), truth_ptr,
+                ctypes.c_void_p(stats.data_ptr()), 0 if chunk_len is None else int(chunk_len),
+                1 if accumulator == "binary16" else 0, n_frames, _stream_ptr(self.device)))
+        return out, stats
+
     def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64) -> torch.Tensor:
         """Host-buffer path (IQ ingest): pinned host IQ -> HBM by chunked
         async copies on a copy stream, pack + correlate on the current stream, taps back

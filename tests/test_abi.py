@@ -24,7 +24,7 @@ def built():
 
 def header_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(pnce_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(pnce_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_matches_binding_table():

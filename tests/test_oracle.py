@@ -153,3 +153,25 @@ def test_noiseless_cfg3(golden):
     assert sha(iq) == str(golden["cfg3_noiseless_iq_sha"])
     est, _, _ = O.process_frames(chips, cfg, O.iq_to_frames(iq))
     assert O.mae(truth, est) == pytest.approx(float(golden["cfg3_noiseless_mae32"]), rel=1e-12)
+
+
+# ------------------------------------------------------------------ tensor16 (f3)
+def _t16():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "t16.npz"))
+
+
+@pytest.mark.parametrize("case", ["b32", "b16", "sat"])
+def test_oracle_tensor16_matches_reference(case):
+    """halfprec.py binary32 / binary16 chunked accumulation, incl. saturation accounting,
+    reproduced by the oracle on the reference's own inputs and estimates."""
+    g = _t16()
+    chunk, acc16 = (int(x) for x in g[f"{case}_cfg"])
+    cfg = O.Config(m=255, c=32, n_t=16, n_batch=4, l=32, n_r=16)
+    chips = O.sequence_for_length(255)
+    for s in range(g[f"{case}_iq"].shape[0]):
+        frames = O.iq_to_frames(g[f"{case}_iq"][s])
+        taps, sats, _ = O.process_frames(chips, cfg, frames, backend="tensor16", chunk_len=chunk,
+                                         accumulator="binary16" if acc16 else "binary32")
+        assert sats == int(g[f"{case}_sat"][s])
+        assert np.array_equal(taps, g[f"{case}_taps"][s])
