@@ -240,6 +240,7 @@ struct CorrParams {
     int32_t raw_prefetch; // raw chunks prefetched into L2 ahead of their load (0 = off)
     int32_t raw_map;      // tm_in is the raw f32 map (L2 prefetch possible in LDG mode)
     int32_t store_hint;   // taps stores with an L2 evict_first policy (default; 0 via knob)
+    int32_t raw_policy;   // L2 policy of the raw-chunk TMA loads (0 evict_first, 1 evict_normal)
     int32_t circ_repl;    // circulant replicas
     int32_t circ_rows;    // rows per replica
     uint32_t stage_bytes;
@@ -870,7 +871,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // ===== raw-chunk producer: TMA the f32 (I,Q) rows of this CTA's 64 links for half a
             // K-block (64 links x 32 samples x 8 B = 16 KB, +16 B per row when C is odd) into the
             // staging ring.  Finer chunks = more loads in flight for the same shared memory.
-            const uint64_t pol = policy_evict_first();
+            // raw rows: consecutive chunks of a row share the 32-byte sector that straddles
+            // them when the row stride is not a sector multiple; the policy decides whether
+            // the second read finds it in L2 (knob PNCE_TUNE_RAW_POLICY: 0 first, 1 normal)
+            const uint64_t pol = p.raw_policy == 1 ? policy_evict_normal() : policy_evict_first();
             int kb = 0, tile = cid, rs = 0;
             int mt = tile / p.n_groups;
             uint32_t rphase = 0;
@@ -1684,6 +1688,8 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.desync_ns = ds ? std::max(0, std::atoi(ds)) : 0;
     const char* sh = std::getenv("PNCE_TUNE_STORE_HINT");
     prm.store_hint = sh ? std::atoi(sh) : 1;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
+    const char* rpol = std::getenv("PNCE_TUNE_RAW_POLICY");
+    prm.raw_policy = rpol ? std::atoi(rpol) : 0;
     const char* rp = std::getenv("PNCE_TUNE_RAW_PREFETCH");
     prm.raw_prefetch = rp ? std::max(0, std::atoi(rp)) : 0;  // measured: L2 prefetch of raw rows only adds traffic
     prm.circ_rows = p->rows_alloc;

@@ -9,6 +9,6 @@ nproc > gpurun_out/host.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_ou
 A="--frames 1024 --gemm-frames 1024 --steps 2 --warmup 3 --no-e2e --no-cpu"
 timeout -s KILL 200 python bench.py $A > gpurun_out/plain_ncu.log 2>&1 && \
 timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py $A > gpurun_out/ncu_launch.log 2>&1; echo "ncu_launch=$?"
-B="--frames 512 --gemm-frames 512 --steps 1 --warmup 3 --no-e2e --no-cpu --no-quality"
+B="--frames 512 --gemm-frames 512 --scored-frames 512 --steps 1 --warmup 3 --no-e2e --no-cpu --file-frames 0"
 timeout -s KILL 200 python bench.py $B > gpurun_out/plain_ncu2.log 2>&1 && \
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_correlate -s 3 -c 2 -o gpurun_out/prof_full python bench.py $B > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_correlate -s 3 -c 6 -o gpurun_out/prof_full python bench.py $B > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
