@@ -93,29 +93,38 @@ __global__ void __launch_bounds__(kSynThreads) k_synth_clean(const float* __rest
         hs[rr * (n_batch * l) + q] = r < n_r ? h[((f * n_r + r) * n_t + t) * l + (q % l)] : make_float2(0.f, 0.f);
     }
     __syncthreads();
+    // all kSynRx receivers of the block per output sample: one chip load feeds 4 complex FMAs
     float pw = 0.f;
-    for (int rr = 0; rr < kSynRx; ++rr) {
-        const int r = rt * kSynRx + rr;
-        if (r >= n_r) break;
-        const float2* hr = hs + rr * (n_batch * l);
-        float2* out = iq + ((f * n_batches + b) * n_r + r) * (int64_t)S;
-        for (int n = threadIdx.x; n < S; n += kSynThreads) {
-            const int l_lo = max(0, n - p + 1), l_hi = min(l - 1, n);
-            float ax = 0.f, ay = 0.f;
-            for (int j = 0; j < n_tx; ++j) {
-                // chip index (n - lag - C - s_j) mod M, walking down with the lag
-                int idx = (n - l_lo - c - spacing * j) % m;
-                if (idx < 0) idx += m;
-                const float2* hj = hr + j * l;
-                for (int lag = l_lo; lag <= l_hi; ++lag) {
-                    const float chip = ch[idx];
-                    ax = fmaf(hj[lag].x, chip, ax);
-                    ay = fmaf(hj[lag].y, chip, ay);
-                    idx = idx == 0 ? m - 1 : idx - 1;
+    const int n_rx = min(kSynRx, n_r - rt * kSynRx);
+    for (int n = threadIdx.x; n < S; n += kSynThreads) {
+        const int l_lo = max(0, n - p + 1), l_hi = min(l - 1, n);
+        float2 acc[kSynRx];
+#pragma unroll
+        for (int rr = 0; rr < kSynRx; ++rr) acc[rr] = make_float2(0.f, 0.f);
+        for (int j = 0; j < n_tx; ++j) {
+            // chip index (n - lag - C - s_j) mod M, walking down with the lag
+            int idx = (n - l_lo - c - spacing * j) % m;
+            if (idx < 0) idx += m;
+            const float2* hj = hs + j * l;
+            for (int lag = l_lo; lag <= l_hi; ++lag) {
+                const float chip = ch[idx];
+#pragma unroll
+                for (int rr = 0; rr < kSynRx; ++rr) {
+                    const float2 hv = hj[rr * (n_batch * l) + lag];
+                    acc[rr].x = fmaf(hv.x, chip, acc[rr].x);
+                    acc[rr].y = fmaf(hv.y, chip, acc[rr].y);
                 }
+                idx = idx == 0 ? m - 1 : idx - 1;
             }
-            out[n] = make_float2(ax, ay);
-            if (n >= c && n < c + m) pw += ax * ax + ay * ay;
+        }
+        const bool body = n >= c && n < c + m;
+#pragma unroll
+        for (int rr = 0; rr < kSynRx; ++rr) {
+            if (rr < n_rx) {
+                const int r = rt * kSynRx + rr;
+                iq[((f * n_batches + b) * n_r + r) * (int64_t)S + n] = acc[rr];
+                if (body) pw += acc[rr].x * acc[rr].x + acc[rr].y * acc[rr].y;
+            }
         }
     }
     // block reduction of the body power -> one float64 atomic per block
