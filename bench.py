@@ -354,6 +354,7 @@ def run_gpu(args, rank, world):
         tg = g0.elapsed_time(g1) / 1e3 / args.steps
         gemm = {"kernel": "k_correlate<packed>", "frames": Fg, "us_per_frame": tg / Fg * 1e6,
                 "tflops": flop_f * Fg / tg / 1e12, "frac_of_bf16_peak": flop_f * Fg / tg / 1e12 / tf_burst,
+                "frac_of_bf16_sustained": (flop_f * Fg / tg / 1e12 / tf_sust) if tf_sust else None,
                 "gbs": bytes_gemm_f * Fg / tg / 1e9}
         del packed
 
@@ -422,6 +423,7 @@ def run_gpu(args, rank, world):
                          "frac": achieved_gbs / hbm, "traffic": traffic,
                          "peak_source": f"{peak_src} HBM copy bandwidth",
                          "tensor_frac": achieved_tf / tf_burst,
+                         "tensor_frac_sustained": (achieved_tf / tf_sust) if tf_sust else None,
                          "algorithmic": {"flop_per_frame": flop_f, "bytes_per_frame": bytes_fused_f,
                                          "bytes": "f32 CP-stripped body in + complex64 taps out",
                                          "frames_per_launch": F}},
