@@ -10,9 +10,11 @@ struct PlanView {
     pnce_cfg_t cfg;
     int n_batches;
     const float* chips;  // device [m], +-1
+    void** synth_cache;  // per-plan state of the synthesiser (owned by pnce_synth.cu)
 };
 
 PlanView plan_view(const pnce_plan_t* plan);
+void synth_cache_free(void* cache);  // called by pnce_plan_destroy
 pnce_status_t set_error(pnce_status_t code, const std::string& msg);
 void count_launch();
 

@@ -1381,10 +1381,13 @@ struct pnce_plan {
     Tiling t16;      // tensor16 emulation: <= 256 columns (multiple of 32), partial + running total
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
+    void* synth = nullptr;  // synthesiser state (pnce_synth.cu)
 };
 
 namespace pnce_internal {
-PlanView plan_view(const pnce_plan_t* p) { return PlanView{p->cfg, p->n_batches, p->chips}; }
+PlanView plan_view(const pnce_plan_t* p) {
+    return PlanView{p->cfg, p->n_batches, p->chips, const_cast<void**>(&p->synth)};
+}
 pnce_status_t set_error(pnce_status_t code, const std::string& msg) { return fail(code, msg); }
 void count_launch() { g_launches++; }
 }  // namespace pnce_internal
@@ -1600,6 +1603,7 @@ pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
     if (!p) return PNCE_OK;
     if (p->chips) cudaFree(p->chips);
     if (p->circ) cudaFree(p->circ);
+    if (p->synth) pnce_internal::synth_cache_free(p->synth);
     delete p;
     return PNCE_OK;
 }
