@@ -82,11 +82,11 @@ __global__ void k_lfsr(int degree, uint32_t tap_mask, uint32_t state0, float* ch
 // Stacked lag-window rows, K-major, zero padded: A[n, k] for n < rows_alloc, k < k_pad.
 template <typename T>
 __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict__ a, int m,
-                                  int k_pad, int r_total, int rows_alloc, int l, int spacing, int repl) {
+                                  int k_pad, int r_total, int rows_alloc, int l, int spacing) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)rows_alloc * k_pad * repl;
+    int64_t total = (int64_t)rows_alloc * k_pad;
     for (; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-        int n = (int)((idx / k_pad) % rows_alloc);
+        int n = (int)(idx / k_pad);
         int k = (int)(idx % k_pad);
         float v = 0.0f;
         if (n < r_total && k < m) {
@@ -236,13 +236,7 @@ struct CorrParams {
     int32_t raw_stages;      // FusedTma: f32 staging ring depth (half-K-block chunks)
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
-    int32_t desync_ns;    // start delay of odd clusters (staggers the epilogue drains)
-    int32_t raw_prefetch; // raw chunks prefetched into L2 ahead of their load (0 = off)
-    int32_t raw_map;      // tm_in is the raw f32 map (L2 prefetch possible in LDG mode)
     int32_t store_hint;   // taps stores with an L2 evict_first policy (default; 0 via knob)
-    int32_t raw_policy;   // L2 policy of the raw-chunk TMA loads (0 evict_first, 1 evict_normal)
-    int32_t circ_repl;    // circulant replicas
-    int32_t circ_rows;    // rows per replica
     uint32_t stage_bytes;
     uint32_t tx_bytes;    // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
@@ -617,17 +611,6 @@ __device__ __noinline__ float recount_nonfinite(const CorrParams& p, const EpiLi
     return bad;
 }
 
-// L2 prefetch of raw chunk `jc` (= 2 * job + half) of this cluster's job list.
-__device__ __forceinline__ void prefetch_raw_chunk(const CorrParams& p, const CUtensorMap* tm, int jc, int jobs,
-                                                   int cid, int n_clusters, uint32_t rank) {
-    const int j = jc >> 1;
-    if (j >= jobs) return;
-    const int ti = j / p.k_blocks;
-    const int kb = j - ti * p.k_blocks;
-    const int mt = (cid + ti * n_clusters) / p.n_groups;
-    tma_prefetch_l2_2d(tm, (2 * (p.c + kb * kBK + (jc & 1) * kRawChunk)) & ~3, (mt * 2 + (int)rank) * kLinksPerTile);
-}
-
 // tensor16 fold (halfprec.py:104-125 on real tensor cores): the accumulation unit just
 // finished in TMEM (binary16 or binary32 partial of one chunk) is widened to fp32, scaled
 // by fp32(1/M) and added to the fp32 running total in TMEM (two roundings, as the
@@ -736,7 +719,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        if (A_TMA || RAW || (FLDG && p.raw_map)) tma_prefetch(&tm_in);
+        if (A_TMA || RAW) tma_prefetch(&tm_in);
         tma_prefetch(&tm_circ);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
@@ -753,22 +736,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const uint32_t a_bytes = kBM * kBK * 2;
     const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
 
-    if (p.desync_ns > 0 && (cid & 1)) {
-        // phase-shift odd clusters so that their store-heavy drains overlap the even
-        // clusters' load-heavy main loops (tiles are equal-length, so the shift persists)
-        uint64_t t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do {
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        } while (t - t0 < (uint64_t)p.desync_ns);
-    }
 
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
             const uint64_t pol_in = policy_evict_first();
             const uint64_t pol_circ = policy_evict_last();
-            const int circ_row0 = (cid % p.circ_repl) * p.circ_rows;
             int kb = 0, tile = cid, stage = 0;
             int mt = tile / p.n_groups, g = tile - mt * p.n_groups;
             uint32_t phase = 0;
@@ -785,7 +758,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
-                                     circ_row0 + g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
+                                     g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
                 if (++kb == p.k_blocks) {
                     kb = 0;
@@ -854,27 +827,11 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #endif
         }
     } else if (warp == 2) {
-        if (FLDG && p.raw_map && p.raw_prefetch > 0 && lane == 0) {
-            // ===== LDG mode: keep the raw rows of the next jobs in L2 (paced by the stages)
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int jc = 0; jc < p.raw_prefetch && jc < 2 * jobs; ++jc)
-                prefetch_raw_chunk(p, &tm_in, jc, jobs, cid, n_clusters, rank);
-            for (int j = 0; j < jobs; ++j) {
-                mbar_wait(&empty[stage], phase ^ 1u);
-                prefetch_raw_chunk(p, &tm_in, 2 * j + p.raw_prefetch, jobs, cid, n_clusters, rank);
-                prefetch_raw_chunk(p, &tm_in, 2 * j + 1 + p.raw_prefetch, jobs, cid, n_clusters, rank);
-                if (++stage == S) { stage = 0; phase ^= 1u; }
-            }
-        }
         if (RAW && lane == 0) {
             // ===== raw-chunk producer: TMA the f32 (I,Q) rows of this CTA's 64 links for half a
             // K-block (64 links x 32 samples x 8 B = 16 KB, +16 B per row when C is odd) into the
             // staging ring.  Finer chunks = more loads in flight for the same shared memory.
-            // raw rows: consecutive chunks of a row share the 32-byte sector that straddles
-            // them when the row stride is not a sector multiple; the policy decides whether
-            // the second read finds it in L2 (knob PNCE_TUNE_RAW_POLICY: 0 first, 1 normal)
-            const uint64_t pol = p.raw_policy == 1 ? policy_evict_normal() : policy_evict_first();
+            const uint64_t pol = policy_evict_first();
             int kb = 0, tile = cid, rs = 0;
             int mt = tile / p.n_groups;
             uint32_t rphase = 0;
@@ -889,8 +846,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     mbar_arrive(&raw_full[rs]);
                     (void)pol; (void)mt; (void)kb;
 #else
-                    if (p.raw_prefetch > 0)
-                        prefetch_raw_chunk(p, &tm_in, 2 * j + h + p.raw_prefetch, jobs, cid, n_clusters, rank);
                     mbar_arrive_expect_tx(&raw_full[rs], p.raw_stage_bytes);
                     // box start rounded down to a 16-byte boundary; converters skip the slack
                     tma_load_2d(raw_base + (size_t)rs * p.raw_stage_bytes, &tm_in, &raw_full[rs],
@@ -1371,9 +1326,7 @@ struct pnce_plan {
     int n_batches;
     int r_total;     // N_b * L
     int k_pad;       // roundup(M, 64)
-    int rows_alloc;  // circulant rows per replica (>= both tilings' coverage)
-    int repl;        // circulant replicas: CTA pairs spread their B loads over replicas so
-                     // the whole grid does not hammer the same L2 lines in lock-step
+    int rows_alloc;  // circulant rows (>= every tiling's coverage)
     int num_sms;
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
     Tiling packed;   // packed operand via TMA: same grouping (TMA ingress, not the drain, bounds G=256)
@@ -1541,9 +1494,7 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    const char* rp = std::getenv("PNCE_TUNE_CIRC_REPL");
-    p->repl = std::max(1, std::min(64, rp ? std::atoi(rp) : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2 * p->repl);
+    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
@@ -1554,14 +1505,14 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         return s;
     }
     const int spacing = cfg->m / cfg->n_batch;
-    const int64_t total = (int64_t)p->rows_alloc * p->k_pad * p->repl;
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
     const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     if (cfg->dtype == PNCE_DTYPE_BF16)
         k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
+            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
     else
         k_build_circulant<__half><<<blocks, 256, 0, st>>>(
-            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing, p->repl);
+            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
     g_launches++;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1569,7 +1520,7 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
     }
-    const uint64_t circ_rows = (uint64_t)p->rows_alloc * p->repl;
+    const uint64_t circ_rows = (uint64_t)p->rows_alloc;
     s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
     if (s == PNCE_OK)
         s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
@@ -1687,16 +1638,8 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     if (m_tiles * t.n_groups > INT32_MAX || 2 * prm.total_links > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
-    prm.circ_repl = p->repl;
-    const char* ds = std::getenv("PNCE_TUNE_DESYNC_NS");
-    prm.desync_ns = ds ? std::max(0, std::atoi(ds)) : 0;
     const char* sh = std::getenv("PNCE_TUNE_STORE_HINT");
     prm.store_hint = sh ? std::atoi(sh) : 1;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
-    const char* rpol = std::getenv("PNCE_TUNE_RAW_POLICY");
-    prm.raw_policy = rpol ? std::atoi(rpol) : 0;
-    const char* rp = std::getenv("PNCE_TUNE_RAW_PREFETCH");
-    prm.raw_prefetch = rp ? std::max(0, std::atoi(rp)) : 0;  // measured: L2 prefetch of raw rows only adds traffic
-    prm.circ_rows = p->rows_alloc;
     prm.n_groups = t.n_groups;
     prm.g_cols = t.g_cols;
     prm.n_mma = t.n_mma;
@@ -1842,7 +1785,6 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (map_ok) {
         s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);
         if (s != PNCE_OK) return s;
-        prm.raw_map = 1;
     }
     if (use_tma) {
         // f32 rows TMA-staged in shared memory (default): A/B ring of up to 3 stages, the
@@ -1886,9 +1828,8 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     } else {
         if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        // tm_in (the raw map) only serves the L2 prefetcher in the LDG variant
-        launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, map_ok ? tm_raw : p->fused.tm_circ,
-                                 p->fused.tm_circ, prm);
+        // the LDG variant reads the rows directly (tm_in unused; the circulant map fills the slot)
+        launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, p->fused.tm_circ, p->fused.tm_circ, prm);
     }
     diag_dump(st);
     g_launches++;
