@@ -400,3 +400,28 @@ def test_lag_layouts(dev, n_t, n_r, m, l, c, nb):
     assert link_err(taps.cpu().numpy(), ref) <= TOL
     packed, _ = corr.correlate(corr.pack(x), 2)
     assert torch.equal(taps, packed)
+
+
+def test_unaligned_buffers(dev):
+    """8-byte (not 16-byte) aligned IQ and taps buffers: the LDG converter path and the
+    scalar-store epilogue path give the same estimates bit for bit."""
+    n, m, l, nb = CONFIGS["cfg2"]
+    cfg, ocfg = make_cfg(n, m, l, nb)
+    _, iq, truth = sim_sets(ocfg, 2)
+    corr = P.Correlator(P.default_spec(8), cfg, n, device=dev)
+    x = torch.from_numpy(iq).to(dev)
+    want, _ = corr.process(x)
+    xb = torch.empty(x.numel() + 2, dtype=torch.float32, device=dev)
+    xu = xb[2:].view(x.shape)                                   # 8-byte offset
+    xu.copy_(x)
+    assert xu.data_ptr() % 16 == 8
+    tb = torch.empty(want.numel() + 1, dtype=torch.complex64, device=dev)
+    tu = tb[1:].view(want.shape)                                # 8-byte offset
+    assert tu.data_ptr() % 16 == 8
+    got, _ = corr.process(xu, out=tu)
+    assert torch.equal(got, want)
+    h = torch.from_numpy(truth.astype(np.complex64)).to(dev)
+    got2, st2, l2 = corr.process_scored(xu, h, out=tu)
+    _, st, lk = corr.process_scored(x, h)
+    assert torch.equal(got2, want)
+    assert torch.allclose(st2, st, rtol=1e-6) and torch.allclose(l2, lk, rtol=1e-6)
