@@ -384,7 +384,8 @@ def run_gpu(args, rank, world):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         e2e = {"value": Fe * world * reps / te * w["n_r"] * w["n_t"], "unit": "CSI estimates/s",
-               "h2d_bytes_per_step": host_iq.numel() * 4, "d2h_bytes_per_step": host_taps.numel() * 8,
+               "h2d_bytes_per_step": Fe * corr.cfg.n_batches * w["n_r"] * w["m"] * 8,   # body-only pitched DMA
+               "d2h_bytes_per_step": host_taps.numel() * 8,
                "frames_per_step": Fe, "us_per_frame": te / (Fe * reps) * 1e6}
 
     # --- IQ-file ingest: reference-format file -> pinned chunks -> HBM ->

@@ -130,6 +130,17 @@ pnce_status_t pnce_process_frames_scored(const pnce_plan_t* plan, const float* i
                                          const float* truth, double* stats, float* link_err,
                                          int64_t n_frames, void* stream);
 
+/* Host-ingest helpers (remove_cp before PCIe, estimator.py:40-47): pnce_copy_bodies_h2d
+ * copies only the CP-stripped bodies of host IQ rows ([F][n_batches][n_r][P+L-1][2] f32,
+ * pinned) into compact device rows of body_stride (>= m) samples with one pitched DMA;
+ * pnce_process_bodies runs the fused estimator (as pnce_process_frames_scored) on such
+ * compact rows. */
+pnce_status_t pnce_copy_bodies_h2d(const pnce_plan_t* plan, const float* iq_host, float* bodies_dev,
+                                   int32_t body_stride, int64_t n_frames, void* stream);
+pnce_status_t pnce_process_bodies(const pnce_plan_t* plan, const float* bodies, int32_t body_stride,
+                                  float* taps, const float* truth, double* stats, float* link_err,
+                                  int64_t n_frames, void* stream);
+
 /* The reference's tensor16 backend on real tensor cores (halfprec.py:93-125):
  * fp16/bf16 operands, the contraction split into chunk_len-sample chunks (0: one chunk;
  * otherwise a multiple of 64 and <= roundup(m, 4)), each chunk accumulated in TMEM as a

@@ -1624,7 +1624,6 @@ static void diag_dump(cudaStream_t st) {
 #endif
 }
 
-static bool c_odd(const pnce_plan_t* p) { return (p->cfg.c & 1) != 0; }
 
 // Shared launch setup for both K3 variants.
 static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fused, float* taps, const float* truth,
@@ -1720,9 +1719,13 @@ struct T16Opts {
     int chunk_kb;
     int acc16;
 };
+// Input row layout override: compact CP-stripped bodies (row stride in samples, no offset)
+struct BodyLayout {
+    int stride;
+};
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                          double* stats, float* link_err, int64_t n_frames, void* stream,
-                                         const T16Opts* t16 = nullptr);
+                                         const T16Opts* t16 = nullptr, const BodyLayout* bodies = nullptr);
 
 pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                   double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
@@ -1737,6 +1740,32 @@ pnce_status_t pnce_process_frames_scored(const pnce_plan_t* p, const float* iq, 
     if (link_err && !truth) return fail(PNCE_ERR_INVALID_CONFIG, "per-link errors need the ground truth");
     if (reinterpret_cast<uintptr_t>(link_err) & 3) return fail(PNCE_ERR_DIMENSION, "link_err must be 4-byte aligned");
     return process_frames_impl(p, iq, taps, truth, stats, link_err, n_frames, stream);
+}
+
+pnce_status_t pnce_process_bodies(const pnce_plan_t* p, const float* bodies, int32_t body_stride, float* taps,
+                                  const float* truth, double* stats, float* link_err, int64_t n_frames, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (body_stride < p->cfg.m) return fail(PNCE_ERR_DIMENSION, "body_stride must be >= m");
+    if (link_err && !truth) return fail(PNCE_ERR_INVALID_CONFIG, "per-link errors need the ground truth");
+    BodyLayout b{body_stride};
+    return process_frames_impl(p, bodies, taps, truth, stats, link_err, n_frames, stream, nullptr, &b);
+}
+
+pnce_status_t pnce_copy_bodies_h2d(const pnce_plan_t* p, const float* iq_host, float* bodies_dev, int32_t body_stride,
+                                   int64_t n_frames, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
+    if (n_frames == 0) return PNCE_OK;
+    if (!iq_host || !bodies_dev) return fail(PNCE_ERR_DIMENSION, "null buffer");
+    if (body_stride < p->cfg.m) return fail(PNCE_ERR_DIMENSION, "body_stride must be >= m");
+    const pnce_cfg_t& c = p->cfg;
+    const int64_t rows = n_frames * p->n_batches * (int64_t)c.n_r;
+    const size_t samples = (size_t)c.c + c.m + c.l - 1;
+    // remove_cp (estimator.py:40-47) as a pitched DMA: only the M body samples cross PCIe
+    CUDA_TRY(cudaMemcpy2DAsync(bodies_dev, (size_t)body_stride * 8, iq_host + 2 * (size_t)c.c, samples * 8,
+                               (size_t)c.m * 8, (size_t)rows, cudaMemcpyHostToDevice,
+                               static_cast<cudaStream_t>(stream)));
+    return PNCE_OK;
 }
 
 pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
@@ -1757,7 +1786,7 @@ pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq
 
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                          double* stats, float* link_err, int64_t n_frames, void* stream,
-                                         const T16Opts* t16) {
+                                         const T16Opts* t16, const BodyLayout* bodies) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
@@ -1770,6 +1799,10 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (s != PNCE_OK) return s;
     prm.iq = iq;
     prm.link_err = link_err;
+    if (bodies) {  // compact bodies: sample k of a link's body at row offset k
+        prm.samples = bodies->stride;
+        prm.c = 0;
+    }
     const bool scored = !t16 && (truth || stats || link_err);
     const int samples = prm.samples;
     const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
@@ -1780,7 +1813,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (t16 && !map_ok)
         return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    prm.raw_row_floats = 2 * kRawChunk + ((c_odd(p)) ? 4 : 0);
+    prm.raw_row_floats = 2 * kRawChunk + ((prm.c & 1) ? 4 : 0);
     CUtensorMap tm_raw;
     if (map_ok) {
         s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);

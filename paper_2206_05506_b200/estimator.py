@@ -248,29 +248,37 @@ class Correlator:
                 1 if accumulator == "binary16" else 0, n_frames, _stream_ptr(self.device)))
         return out, stats
 
-    def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64) -> torch.Tensor:
+    def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64,
+                     bodies_only: bool = True) -> torch.Tensor:
         """Host-buffer path (IQ ingest): pinned host IQ -> HBM by chunked
-        async copies on a copy stream, pack + correlate on the current stream, taps back
-        to pinned host memory on a second copy stream; double-buffered so the PCIe
-        transfers in both directions overlap the device work.  Asynchronous w.r.t. the
-        host: the current stream is made to wait for the final D2H copy."""
+        async copies on a copy stream, correlate on the current stream, taps back to pinned
+        host memory on a second copy stream; double-buffered so the PCIe transfers in both
+        directions overlap the device work.  ``bodies_only``: remove_cp happens in the DMA
+        (a pitched copy of the M body samples per row: 11 % fewer bytes over PCIe at cfg3).
+        Asynchronous w.r.t. the host: the current stream waits for the final D2H copy."""
         if iq_host.is_cuda or taps_host.is_cuda:
             raise DimensionMismatchError("process_host takes host (pinned) tensors")
         n_frames = int(iq_host.shape[0])
         if tuple(iq_host.shape) != self.iq_shape(n_frames) or tuple(taps_host.shape) != self.taps_shape(n_frames):
             raise DimensionMismatchError("host iq/taps shapes do not match the correlator")
+        if not iq_host.is_contiguous() or not taps_host.is_contiguous():
+            raise DimensionMismatchError("host iq/taps must be contiguous")
         if n_frames == 0:
             return taps_host
         chunk = max(1, min(chunk, n_frames))
+        stride = self.cfg.m + (self.cfg.m & 1)       # even: 16-byte aligned compact rows
         cur = torch.cuda.current_stream(self.device)
+        key = (chunk, bodies_only)
         st = getattr(self, "_host_streams", None)
-        if st is None or st[2] != chunk:
-            bufs_in = [torch.empty(self.iq_shape(chunk), dtype=torch.float32, device=self.device) for _ in range(2)]
+        if st is None or st[2] != key:
+            in_shape = (chunk, self.cfg.n_batches, self.n_r, stride, 2) if bodies_only else self.iq_shape(chunk)
+            bufs_in = [torch.empty(in_shape, dtype=torch.float32, device=self.device) for _ in range(2)]
             bufs_out = [torch.empty(self.taps_shape(chunk), dtype=torch.complex64, device=self.device)
                         for _ in range(2)]
-            st = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device), chunk, bufs_in, bufs_out)
+            st = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device), key, bufs_in, bufs_out)
             self._host_streams = st
         s_in, s_out, _, bufs_in, bufs_out = st
+        L = _lib.lib()
         in_done = [torch.cuda.Event() for _ in range(2)]
         comp_done = [torch.cuda.Event() for _ in range(2)]
         out_done = [torch.cuda.Event() for _ in range(2)]
@@ -282,13 +290,24 @@ class Correlator:
             n = min(chunk, n_frames - s)
             if used[b]:
                 s_in.wait_event(comp_done[b])
-            with torch.cuda.stream(s_in):
-                bufs_in[b][:n].copy_(iq_host[s:s + n], non_blocking=True)
+            with torch.cuda.device(self.device), torch.cuda.stream(s_in):
+                if bodies_only:
+                    _lib.check(L.pnce_copy_bodies_h2d(self._plan, ctypes.c_void_p(iq_host[s].data_ptr()),
+                                                      ctypes.c_void_p(bufs_in[b].data_ptr()), stride, n,
+                                                      ctypes.c_void_p(s_in.cuda_stream)))
+                else:
+                    bufs_in[b][:n].copy_(iq_host[s:s + n], non_blocking=True)
                 in_done[b].record(s_in)
             cur.wait_event(in_done[b])
             if used[b]:
                 cur.wait_event(out_done[b])
-            self.process(bufs_in[b][:n], out=bufs_out[b][:n])
+            if bodies_only:
+                with torch.cuda.device(self.device):
+                    _lib.check(L.pnce_process_bodies(self._plan, ctypes.c_void_p(bufs_in[b].data_ptr()), stride,
+                                                     ctypes.c_void_p(bufs_out[b].data_ptr()), None, None, None, n,
+                                                     ctypes.c_void_p(cur.cuda_stream)))
+            else:
+                self.process(bufs_in[b][:n], out=bufs_out[b][:n])
             comp_done[b].record(cur)
             s_out.wait_event(comp_done[b])
             with torch.cuda.stream(s_out):
