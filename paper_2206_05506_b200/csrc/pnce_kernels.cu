@@ -6,14 +6,17 @@
 //       the stacked lag-window rows A[j*L+l, k] = chip[(k - s_j - l) mod M]
 //       (estimator.py:62-65,114-117) as an fp16/bf16 K-major operand.
 //   K2  k_pack_iq : remove_cp (estimator.py:40-47) + de-interleave + quantise the
-//       received f32 (I,Q) samples into rows (frame, batch, rx, re|im) x K.
-//   K3  k_correlate : tcgen05 UMMA  D^T[rows, R] = B^T[rows, K] . A^T[K, R]
-//       (both real GEMMs of estimator.py:77-80 in one contraction; the huge
-//       frame x rx x re/im axis is the UMMA M dimension), TMA-fed, warp-specialised,
-//       persistent, TMEM double-buffered accumulator.
-//   K4  (fused into K3's epilogue) x 1/M, Re/Im pairing, per-transmitter window
-//       demux into taps[f, r, t, l] (experiments.py:206-207) and optional
-//       sum|e|, sum|e|^2, non-finite count vs. truth (metrics.py:19-25 + MSE).
+//       received f32 (I,Q) samples into rows (frame, batch, rx, re|im) x K (two-pass path).
+//   K3  k_correlate<MODE, SCORED, EPI8, T16> : tcgen05 CTA-pair UMMA
+//       D[rows, lags] = X[rows, K] . C[lags, K]^T (both real GEMMs of estimator.py:77-80 in
+//       one contraction; the frame x batch x rx x re/im axis is the UMMA M dimension);
+//       MODE 2 converts the f32 rows itself (TMA-staged chunks -> fp16/bf16 A stages), so
+//       K2 is fused away; warp-specialised, persistent, mbarrier pipelines, accumulators
+//       in TMEM (512 columns at cfg3, single-buffered).
+//   K4  (K3's epilogue) x 1/M, per-transmitter window demux into taps[f, r, t, l]
+//       (experiments.py:206-207), optional sum|e|, sum|e|^2, non-finite count and per-link
+//       MSE vs. truth (metrics.py:19-25 + MSE), or the tensor16 chunk fold (halfprec.py).
+// DESIGN.md §5 has the layouts, rooflines and measurements.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
