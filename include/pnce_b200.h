@@ -91,6 +91,16 @@ pnce_status_t pnce_generate_mseq(int32_t degree, uint32_t tap_mask, uint32_t sta
 pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** plan, void* stream);
 pnce_status_t pnce_plan_destroy(pnce_plan_t* plan);
 
+/* Operator-level seam: a plan over caller-supplied correlation rows, the `rows` argument of
+ * correlate_rows (estimator.py:68-86; build_partial_circulant / batched_lag_rows output).
+ * rows_dev: float32 [n_rows][m] on the device (+-1 for PN rows; any values are rounded to
+ * the plan dtype), 1 <= n_rows <= m (RowsOutOfRange otherwise); norm_len: the 1/norm_len
+ * scale.  From cfg only m, n_r (received columns) and dtype are used.  Correlating y
+ * ([n_r] columns of m samples) is pnce_process_bodies with body rows of y's columns:
+ * taps[f][col][0][q] = (1/norm_len) sum_k rows[q][k] y[k][col]. */
+pnce_status_t pnce_plan_create_rows(const pnce_cfg_t* cfg, const float* rows_dev, int32_t n_rows,
+                                    int32_t norm_len, pnce_plan_t** plan, void* stream);
+
 /* Copy the plan's device-generated chips (float32 [m]) into dst_dev. */
 pnce_status_t pnce_plan_chips(const pnce_plan_t* plan, float* dst_dev, void* stream);
 

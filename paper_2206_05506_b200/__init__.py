@@ -7,7 +7,9 @@ compute runs in libpnce_b200.so (sm_100a tcgen05/TMA kernels) via a C ABI.
 from .errors import *  # noqa: F401,F403
 from .estimator import (CirEstimate, Correlator, WorkCounters, correlator_rows_for_plan,  # noqa: F401
                         process_frames, remove_cp)
-from . import iqfile, sweeps, synth  # noqa: F401
+from . import iqfile, operators, sweeps, synth  # noqa: F401
+from .operators import (RowsCorrelator, batched_lag_rows, build_partial_circulant, correlate_rows,  # noqa: F401
+                        estimate_batched, estimate_sequential, validate_batch_separation)
 from .metrics import mae, mse  # noqa: F401
 from .pilots import (BatchAssignment, BatchPlan, PilotConfig, build_batch_plan,  # noqa: F401
                      cyclic_separation, max_batch, propagation_time, shift_for_transmitter)

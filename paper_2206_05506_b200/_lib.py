@@ -34,7 +34,7 @@ _STATUS = {
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
     "pnce_version", "pnce_last_error", "pnce_config_check", "pnce_generate_mseq",
-    "pnce_plan_create", "pnce_plan_destroy", "pnce_plan_chips", "pnce_workspace_bytes",
+    "pnce_plan_create", "pnce_plan_create_rows", "pnce_plan_destroy", "pnce_plan_chips", "pnce_workspace_bytes",
     "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored",
     "pnce_process_frames_tensor16", "pnce_copy_bodies_h2d", "pnce_process_bodies", "pnce_draw_channel", "pnce_simulate_frames", "pnce_kernel_launches",
 )
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
         "pnce_config_check": (i32, [cfgp]),
         "pnce_generate_mseq": (i32, [i32, ctypes.c_uint32, ctypes.c_uint32, vp, i32, vp]),
         "pnce_plan_create": (i32, [cfgp, ctypes.POINTER(vp), vp]),
+        "pnce_plan_create_rows": (i32, [cfgp, vp, i32, i32, ctypes.POINTER(vp), vp]),
         "pnce_plan_destroy": (i32, [vp]),
         "pnce_plan_chips": (i32, [vp, vp, vp]),
         "pnce_workspace_bytes": (sz, [vp, i64]),

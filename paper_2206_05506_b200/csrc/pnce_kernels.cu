@@ -105,6 +105,22 @@ __global__ void k_build_circulant(const float* __restrict__ chips, T* __restrict
     }
 }
 
+// Caller-supplied correlation rows (correlate_rows' `rows`, estimator.py:68-86) as the
+// K-major operand: rows [n_rows][m] f32 -> [rows_alloc][k_pad] fp16/bf16 (RN), zero padded.
+template <typename T>
+__global__ void k_rows_to_operand(const float* __restrict__ rows, T* __restrict__ a, int m, int k_pad, int n_rows,
+                                  int rows_alloc) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)rows_alloc * k_pad;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(idx / k_pad), k = (int)(idx % k_pad);
+        const float v = (n < n_rows && k < m) ? rows[(int64_t)n * m + k] : 0.f;
+        if constexpr (std::is_same<T, __half>::value)
+            a[idx] = __float2half_rn(v);
+        else
+            a[idx] = __float2bfloat16_rn(v);
+    }
+}
+
 // ------------------------------------------------------------------ K2: pack
 // Packed-operand row order (shared with the fused converters): links are grouped by 8 and
 // each 16-row block holds the 8 Re rows then the 8 Im rows, so that the 16x256b TMEM load
@@ -1338,6 +1354,7 @@ struct pnce_plan {
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
     void* synth = nullptr;  // synthesiser state (pnce_synth.cu)
+    float inv_norm = 0.f;   // 1 / norm_len (correlate_rows' norm_len; M for PN plans)
 };
 
 namespace pnce_internal {
@@ -1401,6 +1418,68 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
         k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
     else
         k_correlate<MODE, false><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+}
+
+// Tilings, operand rows and tensor maps of a plan: the PN lag-window rows built from the
+// plan's chips (rows == nullptr) or caller-supplied rows [r_total][m] f32 (device).
+static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st) {
+    const pnce_cfg_t& cfg = p->cfg;
+    p->k_pad = (cfg.m + kBK - 1) / kBK * kBK;
+    // Tuning knobs (diagnostics): maximum accumulator columns per lag-row group.
+    const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
+    const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
+    make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
+    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
+    const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
+    make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
+    make_tiling(p->t16, p->r_total, 256, 32);  // 32-column fold chunks
+    p->t16.acc_stages = 1;
+    p->t16.tmem_cols = 512;
+    p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
+                              p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols});
+    cudaError_t e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
+    if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
+    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    const bool bf16 = cfg.dtype == PNCE_DTYPE_BF16;
+    if (rows) {
+        if (bf16)
+            k_rows_to_operand<__nv_bfloat16><<<blocks, 256, 0, st>>>(rows, (__nv_bfloat16*)p->circ, cfg.m, p->k_pad,
+                                                                      p->r_total, p->rows_alloc);
+        else
+            k_rows_to_operand<__half><<<blocks, 256, 0, st>>>(rows, (__half*)p->circ, cfg.m, p->k_pad, p->r_total,
+                                                               p->rows_alloc);
+    } else {
+        const int spacing = cfg.m / cfg.n_batch;
+        if (bf16)
+            k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+                p->chips, (__nv_bfloat16*)p->circ, cfg.m, p->k_pad, p->r_total, p->rows_alloc, cfg.l, spacing);
+        else
+            k_build_circulant<__half><<<blocks, 256, 0, st>>>(p->chips, (__half*)p->circ, cfg.m, p->k_pad,
+                                                               p->r_total, p->rows_alloc, cfg.l, spacing);
+    }
+    g_launches++;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("operand rows: ") + cudaGetErrorString(e));
+    const uint64_t circ_rows = (uint64_t)p->rows_alloc;
+    pnce_status_t s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, bf16);
+    if (s == PNCE_OK) s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2, bf16);
+    if (s == PNCE_OK) s = make_tmap(&p->t16.tm_circ, p->circ, p->k_pad, circ_rows, p->t16.nm / 2, bf16);
+    if (s == PNCE_OK)
+        s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2, bf16);
+    if (s != PNCE_OK) return s;
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_err = set_smem_attrs<kModePacked>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedLdg>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedTma>();
+        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModePackedLdg>();
+    });
+    if (attr_err != cudaSuccess)
+        return fail(PNCE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return PNCE_OK;
 }
 
 extern "C" {
@@ -1480,74 +1559,54 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
     p->cfg = *cfg;
     p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
     p->r_total = cfg->n_batch * cfg->l;
-    p->k_pad = (cfg->m + kBK - 1) / kBK * kBK;
-    // Tuning knobs (diagnostics): maximum accumulator columns per lag-row group.
-    const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
-    const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
-    make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
-    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
-    const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
-    make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
-    make_tiling(p->t16, p->r_total, 256, 32);  // 32-column fold chunks
-    p->t16.acc_stages = 1;
-    p->t16.tmem_cols = 512;
-    p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
-                              p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols});
     p->num_sms = sms;
-
+    p->inv_norm = 1.0f / (float)cfg->m;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMalloc(&p->chips, sizeof(float) * cfg->m);
-    if (e == cudaSuccess) e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
     if (e != cudaSuccess) {
         pnce_plan_destroy(p);
         return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
     }
     s = pnce_generate_mseq(cfg->degree, cfg->tap_mask, cfg->state, p->chips, cfg->m, stream);
+    if (s == PNCE_OK) s = plan_build(p, nullptr, st);
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
         return s;
     }
-    const int spacing = cfg->m / cfg->n_batch;
-    const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
-    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    if (cfg->dtype == PNCE_DTYPE_BF16)
-        k_build_circulant<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-            p->chips, (__nv_bfloat16*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
-    else
-        k_build_circulant<__half><<<blocks, 256, 0, st>>>(
-            p->chips, (__half*)p->circ, cfg->m, p->k_pad, p->r_total, p->rows_alloc, cfg->l, spacing);
-    g_launches++;
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-        pnce_plan_destroy(p);
-        return fail(PNCE_ERR_CUDA, std::string("k_build_circulant: ") + cudaGetErrorString(e));
-    }
-    const uint64_t circ_rows = (uint64_t)p->rows_alloc;
-    s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
-    if (s == PNCE_OK)
-        s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2,
-                      cfg->dtype == PNCE_DTYPE_BF16);
-    if (s == PNCE_OK)
-        s = make_tmap(&p->t16.tm_circ, p->circ, p->k_pad, circ_rows, p->t16.nm / 2, cfg->dtype == PNCE_DTYPE_BF16);
-    if (s == PNCE_OK)
-        s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2,
-                      cfg->dtype == PNCE_DTYPE_BF16);
+    *out = p;
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_plan_create_rows(const pnce_cfg_t* cfg, const float* rows, int32_t n_rows, int32_t norm_len,
+                                    pnce_plan_t** out, void* stream) {
+    if (!out) return fail(PNCE_ERR_INVALID_CONFIG, "null plan out-pointer");
+    *out = nullptr;
+    if (!cfg || !rows) return fail(PNCE_ERR_INVALID_CONFIG, "null config or rows");
+    if (cfg->m < 1 || cfg->n_r < 1) return fail(PNCE_ERR_DIMENSION, "m and n_r must be >= 1");
+    if (n_rows < 1 || n_rows > cfg->m) return fail(PNCE_ERR_ROWS_OUT_OF_RANGE, "row count outside [1, M]");
+    if (norm_len < 1) return fail(PNCE_ERR_INVALID_CONFIG, "norm_len must be >= 1");
+    if (cfg->dtype != PNCE_DTYPE_FP16 && cfg->dtype != PNCE_DTYPE_BF16)
+        return fail(PNCE_ERR_INVALID_CONFIG, "dtype must be fp16 or bf16");
+    int dev = 0, major = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return fail(PNCE_ERR_UNSUPPORTED_DEVICE, "pnce_b200 needs an sm_100 (B200) device");
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // one "batch" of one "transmitter" whose window is the whole row set: taps[f][r][0][q] = row q
+    pnce_plan* p = new pnce_plan();
+    p->cfg = *cfg;
+    p->cfg.c = 0;
+    p->cfg.l = n_rows;
+    p->cfg.n_t = 1;
+    p->cfg.n_batch = 1;
+    p->n_batches = 1;
+    p->r_total = n_rows;
+    p->num_sms = sms;
+    p->inv_norm = 1.0f / (float)norm_len;
+    pnce_status_t s = plan_build(p, rows, static_cast<cudaStream_t>(stream));
     if (s != PNCE_OK) {
         pnce_plan_destroy(p);
         return s;
-    }
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_err = set_smem_attrs<kModePacked>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedLdg>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedTma>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModePackedLdg>();
-    });
-    if (attr_err != cudaSuccess) {
-        pnce_plan_destroy(p);
-        return fail(PNCE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     }
     *out = p;
     return PNCE_OK;
@@ -1564,6 +1623,7 @@ pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
 
 pnce_status_t pnce_plan_chips(const pnce_plan_t* p, float* dst, void* stream) {
     if (!p || !dst) return fail(PNCE_ERR_INVALID_CONFIG, "null plan or destination");
+    if (!p->chips) return fail(PNCE_ERR_INVALID_CONFIG, "plan was built from caller rows (no PN chips)");
     CUDA_TRY(cudaMemcpyAsync(dst, p->chips, sizeof(float) * p->cfg.m, cudaMemcpyDeviceToDevice,
                              static_cast<cudaStream_t>(stream)));
     return PNCE_OK;
@@ -1663,7 +1723,7 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.c = c.c;
     prm.samples = c.c + c.m + c.l - 1;
     prm.bf16 = c.dtype == PNCE_DTYPE_BF16;
-    prm.inv_m = 1.0f / (float)c.m;
+    prm.inv_m = p->inv_norm;
     prm.inv_l = 1.0f / (float)c.l;
     prm.k_pad = p->k_pad;
     prm.chunk_kb = prm.k_blocks;

@@ -269,6 +269,7 @@ pnce_status_t pnce_simulate_frames(const pnce_plan_t* plan, const float* h, doub
     using pnce_internal::set_error;
     if (!plan) return set_error(PNCE_ERR_INVALID_CONFIG, "null plan");
     const PlanView v = pnce_internal::plan_view(plan);
+    if (!v.chips) return set_error(PNCE_ERR_INVALID_CONFIG, "synthesis needs a PN plan (pnce_plan_create)");
     if (n_frames < 0) return set_error(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
     if (!h || !iq || (reinterpret_cast<uintptr_t>(h) & 7) || (reinterpret_cast<uintptr_t>(iq) & 7))
