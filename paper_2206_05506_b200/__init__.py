@@ -11,9 +11,9 @@ from . import iqfile, operators, sweeps, synth  # noqa: F401
 from .operators import (RowsCorrelator, batched_lag_rows, build_partial_circulant, correlate_rows,  # noqa: F401
                         estimate_batched, estimate_sequential, validate_batch_separation)
 from .metrics import mae, mse  # noqa: F401
-from .pilots import (BatchAssignment, BatchPlan, PilotConfig, build_batch_plan,  # noqa: F401
-                     cyclic_separation, max_batch, propagation_time, shift_for_transmitter)
-from .pn import (PRIMITIVE_TAPS, LfsrSpec, PnSequence, default_spec, generate_mseq,  # noqa: F401
-                 sequence_for_length)
+from .pilots import (BatchAssignment, BatchPlan, PilotConfig, PilotFrame, build_batch_plan,  # noqa: F401
+                     build_pilot, cyclic_separation, max_batch, propagation_time, shift_for_transmitter)
+from .pn import (PRIMITIVE_TAPS, LfsrSpec, PnSequence, circular_autocorrelation, circular_shift,  # noqa: F401
+                 default_spec, generate_mseq, sequence_for_length)
 
 __version__ = "0.1.0"

@@ -107,3 +107,22 @@ def sequence_for_length(m: int, device=None) -> PnSequence:
     if (1 << degree) - 1 != m:
         raise InvalidSpecError(f"PN length {m} is not 2**k - 1")
     return generate_mseq(default_spec(degree), device)
+
+
+def circular_autocorrelation(seq: PnSequence, lag: int) -> float:
+    """pn.py:141-146: (1/M) sum_m s[m] s[(m + lag) mod M]."""
+    from .errors import LagOutOfRangeError
+    m = seq.m
+    if not 0 <= lag < m:
+        raise LagOutOfRangeError(f"lag {lag} outside [0, {m})")
+    c = seq.chips.double()
+    return float(torch.dot(c, torch.roll(c, -lag)).item() / m)
+
+
+def circular_shift(seq: PnSequence, shift: int) -> PnSequence:
+    """pn.py:149-160: cyclic delay by ``shift`` chips (chip 0 moves to index ``shift``)."""
+    from .errors import ShiftOutOfRangeError
+    m = seq.m
+    if not 0 <= shift < m:
+        raise ShiftOutOfRangeError(f"shift {shift} outside [0, {m})")
+    return PnSequence(chips=torch.roll(seq.chips, shift), spec=seq.spec)

@@ -50,3 +50,46 @@ def test_remove_cp_and_errors():
     assert list(P.remove_cp(np.arange(10.0), 3, 7)) == list(np.arange(3.0, 10.0))
     with pytest.raises(P.FrameTooShortError):
         P.remove_cp(np.zeros(9), 3, 7)
+
+
+# ---------------------------------------------------------------- pn / pilot helpers (CPU tensors)
+def _cpu_seq(degree):
+    import torch
+
+    from oracle import pnce_oracle as O
+    from paper_2206_05506_b200 import PnSequence, default_spec
+    taps = O.taps_for_degree(degree)
+    return PnSequence(chips=torch.from_numpy(O.generate_mseq(degree, taps, 1)).float(), spec=default_spec(degree))
+
+
+def test_circular_autocorrelation_two_valued():
+    """test_pn.py: m-sequences have R(0) = 1 and R(lag) = -1/M elsewhere."""
+    import pytest
+
+    import paper_2206_05506_b200 as P
+    seq = _cpu_seq(9)
+    assert P.circular_autocorrelation(seq, 0) == 1.0
+    for lag in (1, 2, 100, 510):
+        assert abs(P.circular_autocorrelation(seq, lag) + 1 / 511) < 1e-12
+    with pytest.raises(P.LagOutOfRangeError):
+        P.circular_autocorrelation(seq, 511)
+
+
+def test_circular_shift_and_pilot():
+    """pn.py:149-160 delay semantics and pilots.py:103-110 against the oracle's build_pilot."""
+    import numpy as np
+    import pytest
+
+    import paper_2206_05506_b200 as P
+    from oracle import pnce_oracle as O
+    seq = _cpu_seq(8)
+    s = P.circular_shift(seq, 5)
+    assert s.chips[5].item() == seq.chips[0].item()
+    assert np.array_equal(P.circular_shift(s, 7).chips.numpy(), P.circular_shift(seq, 12).chips.numpy())
+    with pytest.raises(P.ShiftOutOfRangeError):
+        P.circular_shift(seq, 255)
+    pf = P.build_pilot(seq, 63, 32, transmitter=1)
+    assert len(pf) == 32 + 255 and pf.transmitter == 1 and pf.shift == 63
+    assert np.array_equal(pf.samples.double().numpy(), O.build_pilot(seq.chips.double().numpy(), 63, 32))
+    with pytest.raises(P.InvalidConfigError):
+        P.build_pilot(seq, 0, 0)
