@@ -1121,7 +1121,11 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
             // (links are re-derived where needed instead of kept live: register pressure)
             const int n0 = g * p.g_cols + colp;
+#ifndef PNCE_DIAG_NO_TRUTH_PF
             if (SCORED && p.truth != nullptr && (lane & 3) == 0) {
+#else
+            if (false) {
+#endif
                 // pull this tile's truth windows into L2 while the MMAs run
                 for (int k = 0; k < kBlocksPerWarp; ++k) {
                     const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
@@ -1349,7 +1353,7 @@ struct pnce_plan {
     int num_sms;
     Tiling fused;    // f32 IQ in: prefer one group (<= 512 cols) so samples are converted once
     Tiling packed;   // packed operand via TMA: same grouping (TMA ingress, not the drain, bounds G=256)
-    Tiling packed_ldg;  // packed operand via LDG: <= 256 columns, double-buffered accumulator
+    Tiling packed_ldg;  // <= 256 columns, double-buffered accumulator (packed LDG mode, scored launches)
     Tiling t16;      // tensor16 emulation: <= 256 columns (multiple of 32), partial + running total
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
@@ -1856,9 +1860,16 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
     CorrParams prm;
-    // tensor16: scoring moves to the finish kernel (saturated batches are scored as zeros)
-    pnce_status_t s = fill_params(p, t16 ? p->t16 : p->fused, true, taps, t16 ? nullptr : truth,
-                                  t16 ? nullptr : stats, n_frames, prm);
+    // tensor16: scoring moves to the finish kernel (saturated batches are scored as zeros).
+    // Scored launches (drain ~2x the main loop) use <= 256-column groups with two TMEM
+    // accumulators, so one tile's drain overlaps the next tile's MMAs (knob PNCE_TUNE_SCORED_G)
+    const bool scored_launch = !t16 && (truth || stats || link_err);
+    static const int scored_g = [] {
+        const char* e = std::getenv("PNCE_TUNE_SCORED_G");
+        return e ? std::atoi(e) : 256;
+    }();
+    const Tiling& tiling = t16 ? p->t16 : (scored_launch && scored_g == 256 ? p->packed_ldg : p->fused);
+    pnce_status_t s = fill_params(p, tiling, true, taps, t16 ? nullptr : truth, t16 ? nullptr : stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
     prm.link_err = link_err;
@@ -1919,13 +1930,13 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             cudaFreeAsync(flags, st);
             if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16: ") + cudaGetErrorString(e));
         } else {
-            launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, p->fused.tm_circ, prm);
+            launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, tiling.tm_circ, prm);
         }
     } else {
         if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         // the LDG variant reads the rows directly (tm_in unused; the circulant map fills the slot)
-        launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, p->fused.tm_circ, p->fused.tm_circ, prm);
+        launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, tiling.tm_circ, tiling.tm_circ, prm);
     }
     diag_dump(st);
     g_launches++;
