@@ -245,6 +245,77 @@ def run_tap_sweep(cfg: ExperimentConfig, device=None, group=None) -> list[SweepR
     return _run(cfg, tap_sweep_points(cfg), device, group)
 
 
+@dataclass
+class BenchPoint:
+    """experiments.py:112-131: latency statistics of one (M, N_batch) point."""
+
+    backend: str
+    n_t: int
+    n_r: int
+    m: int
+    c: int
+    l: int
+    l_nz: int
+    n_batch: int
+    snr_db: float
+    reps: int
+    mean_s: float
+    std_s: float
+    median_s: float
+    samples_moved: int
+    macs: int
+    seed: int
+    times_s: tuple = ()
+
+
+@dataclass
+class LatencyReport:
+    points: list
+
+
+def run_latency_bench(cfg: ExperimentConfig, reps: int = 10, warmup: int = 2, device=None) -> LatencyReport:
+    """experiments.py:351-408 on the device: per-frame-set processing time (CUDA events around
+    one fused launch on a resident synthesised frame-set) over the (M, N_batch) grid."""
+    import statistics
+
+    from . import synth
+    if reps < 1:
+        raise InvalidConfigError("reps must be >= 1")
+    if device is None:
+        device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
+    points = []
+    for m in cfg.pn_lengths:
+        for nb in cfg.n_batch:
+            corr = _correlator(cfg, m, nb, device)
+            cs, ns = derive_seeds(cfg.seed, m, nb, 0)
+            h = synth.draw_channel(corr, 1, l_nz=cfg.l_nz[0], seed=cs)
+            iq = synth.simulate_frames(corr, h, cfg.snr_db[0], seed=ns)
+            taps = torch.empty(corr.taps_shape(1), dtype=torch.complex64, device=device)
+            times = []
+            for rep in range(warmup + reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                corr.process(iq, out=taps)
+                e1.record()
+                torch.cuda.synchronize(device)
+                if rep >= warmup:
+                    times.append(e0.elapsed_time(e1) / 1e3)
+            pil = corr.cfg
+            points.append(BenchPoint(f"tcgen05-{cfg.backend}", cfg.n_t, cfg.n_r, m, cfg.c, cfg.l, cfg.l_nz[0], nb,
+                                     cfg.snr_db[0], len(times), statistics.fmean(times),
+                                     statistics.stdev(times) if len(times) > 1 else 0.0, statistics.median(times),
+                                     pil.n_batches * cfg.n_r * pil.p, cfg.n_t * cfg.l * m * cfg.n_r, cfg.seed,
+                                     tuple(times)))
+    return LatencyReport(points=points)
+
+
+def bench_rows(report: LatencyReport, record_latency: bool = True) -> list[SweepResult]:
+    """experiments.py:410-435: CSV-schema rows (mae column zeroed)."""
+    return [SweepResult("latency_bench", p.backend, p.n_t, p.n_r, p.m, p.c, p.l, p.l_nz, p.n_batch, p.snr_db, p.reps,
+                        p.seed, 0.0, p.mean_s if record_latency else 0.0, p.samples_moved, p.macs, 0)
+            for p in report.points]
+
+
 def main(argv=None) -> int:
     """`python -m paper_2206_05506_b200.sweeps` (torchrun for several GPUs): the reference CLI's
     `snr-sweep` / `tap-sweep` on the device, CSV on rank 0."""
@@ -252,7 +323,7 @@ def main(argv=None) -> int:
 
     import torch.distributed as dist
     ap = argparse.ArgumentParser(description=main.__doc__)
-    ap.add_argument("experiment", choices=["snr", "tap"])
+    ap.add_argument("experiment", choices=["snr", "tap", "bench"])
     ap.add_argument("--out", default="-")
     ap.add_argument("--nt", type=int, default=16)
     ap.add_argument("--nr", type=int, default=16)
@@ -274,7 +345,11 @@ def main(argv=None) -> int:
     cfg = ExperimentConfig(n_t=a.nt, n_r=a.nr, pn_lengths=tuple(a.m), c=a.c, l=a.l,
                            l_nz=tuple(a.l_nz or [a.l]), n_batch=tuple(a.n_batch), snr_db=tuple(a.snr),
                            iterations=a.iterations, seed=a.seed, backend=a.dtype, emit_per_iteration=a.per_iteration)
-    rows = (run_snr_sweep if a.experiment == "snr" else run_tap_sweep)(cfg)
+    if a.experiment == "bench":
+        rank0 = not dist.is_initialized() or dist.get_rank() == 0
+        rows = bench_rows(run_latency_bench(cfg)) if rank0 else None
+    else:
+        rows = (run_snr_sweep if a.experiment == "snr" else run_tap_sweep)(cfg)
     if rows is not None:
         text = render_csv(rows)
         if a.out == "-":

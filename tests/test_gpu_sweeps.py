@@ -58,3 +58,16 @@ def test_cfg2_mae_curve(dev):
     for k, r in enumerate(head):
         its = per_it[64 * k:64 * (k + 1)]
         assert math.isclose(r.mae, math.fsum(x.mae for x in its) / 64, rel_tol=1e-12)
+
+
+def test_latency_bench_rows(dev):
+    cfg = SW.ExperimentConfig(n_t=16, n_r=16, pn_lengths=(255, 511), c=32, l=32, l_nz=(32,), n_batch=(1, 4),
+                              snr_db=(10.0,), iterations=1, seed=0)
+    rep = SW.run_latency_bench(cfg, reps=3, warmup=1, device=dev)
+    assert [(p.m, p.n_batch) for p in rep.points] == [(255, 1), (255, 4), (511, 1), (511, 4)]
+    rows = SW.bench_rows(rep)
+    assert all(r.experiment == "latency_bench" and r.mae == 0.0 and r.latency_s > 0 and r.iterations == 3
+               for r in rows)
+    assert rows[0].macs == 16 * 32 * 255 * 16 and rows[0].samples_moved == 16 * 16 * (32 + 255)
+    text = SW.render_csv(rows)
+    assert SW.render_csv(SW.parse_csv(text)) == text
