@@ -30,7 +30,16 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json configs[2] (headline single-GPU bench)
 WORKLOAD = dict(name="cfg3", n_t=64, n_r=64, m=1023, l=64, c=64, n_batch=8, snr_db=10.0)
-METRIC = "CSI estimates/sec & us/frame at 64x64 MIMO, PN 1023; tensor-pipe % of peak"
+def _baseline_metric() -> str:
+    """BASELINE.json's metric string, verbatim (fallback: the same text)."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "BASELINE.json")) as fh:
+            return json.load(fh)["metric"]
+    except Exception:
+        return "CSI estimates/sec & \u00b5s/frame at 64\u00d764 MIMO, PN 1023; tensor-pipe % of peak"
+
+
+METRIC = _baseline_metric()
 
 
 def load_peaks():
