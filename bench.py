@@ -375,7 +375,7 @@ def run_gpu(args, rank, world):
         host_iq.copy_(iq[:Fe].cpu())
         host_taps = torch.empty(corr.taps_shape(Fe), dtype=torch.complex64).pin_memory()
         for _ in range(2):
-            corr.process_host(host_iq, host_taps)
+            corr.process_host(host_iq, host_taps, chunk=args.e2e_chunk)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -384,7 +384,7 @@ def run_gpu(args, rank, world):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(reps):
-            corr.process_host(host_iq, host_taps)
+            corr.process_host(host_iq, host_taps, chunk=args.e2e_chunk)
         t1.record(stream)
         torch.cuda.synchronize(dev)
         te = t0.elapsed_time(t1) / 1e3
@@ -395,7 +395,7 @@ def run_gpu(args, rank, world):
         e2e = {"value": Fe * world * reps / te * w["n_r"] * w["n_t"], "unit": "CSI estimates/s",
                "h2d_bytes_per_step": Fe * corr.cfg.n_batches * w["n_r"] * w["m"] * 8,   # body-only pitched DMA
                "d2h_bytes_per_step": host_taps.numel() * 8,
-               "frames_per_step": Fe, "us_per_frame": te / (Fe * reps) * 1e6}
+               "frames_per_step": Fe, "chunk": args.e2e_chunk, "us_per_frame": te / (Fe * reps) * 1e6}
 
     # --- IQ-file ingest: reference-format file -> pinned chunks -> HBM ->
     # taps in pinned host memory (N=1 only: a host-I/O leg with per-rank temp files)
@@ -455,6 +455,7 @@ def main():
     ap.add_argument("--frames", type=int, default=10000, help="frame-sets per step per GPU")
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--e2e-frames", type=int, default=512)
+    ap.add_argument("--e2e-chunk", type=int, default=8, help="frame-sets per H2D/compute/D2H pipeline stage")
     ap.add_argument("--file-frames", type=int, default=256, help="frame-sets in the IQ-file ingest leg (0: off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -248,7 +248,7 @@ class Correlator:
                 1 if accumulator == "binary16" else 0, n_frames, _stream_ptr(self.device)))
         return out, stats
 
-    def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 64,
+    def process_host(self, iq_host: torch.Tensor, taps_host: torch.Tensor, chunk: int = 8,
                      bodies_only: bool = True) -> torch.Tensor:
         """Host-buffer path (IQ ingest): pinned host IQ -> HBM by chunked
         async copies on a copy stream, correlate on the current stream, taps back to pinned
