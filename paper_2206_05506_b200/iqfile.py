@@ -145,8 +145,9 @@ def _check_geometry(header: IqFileHeader, corr) -> int:
 
 
 _POOL = None
-_READ_THREADS = max(1, min(8, (os.cpu_count() or 1)))
-_PIECE = 32 << 20
+_READ_THREADS = max(1, min(16, (os.cpu_count() or 1)))
+_PIECE = 8 << 20          # upper bound; a read is split so every reader thread gets a piece
+_MIN_PIECE = 1 << 20
 
 
 def _pread_into(fd: int, view: memoryview, offset: int) -> None:
@@ -162,7 +163,9 @@ def _parallel_read(fd: int, view: memoryview, offset: int) -> None:
     """Page-cache/NVMe -> pinned memory with several threads (a single memcpy-bound reader
     tops out near 6-7 GB/s; preadv releases the GIL)."""
     global _POOL
-    pieces = [(s, min(len(view), s + _PIECE)) for s in range(0, len(view), _PIECE)]
+    piece = min(_PIECE, max(_MIN_PIECE, -(-len(view) // _READ_THREADS)))
+    piece = -(-piece // 4096) * 4096
+    pieces = [(s, min(len(view), s + piece)) for s in range(0, len(view), piece)]
     if len(pieces) <= 1 or _READ_THREADS == 1:
         _pread_into(fd, view, offset)
         return
@@ -184,7 +187,7 @@ def load_iq(path, corr, pin: bool = True) -> torch.Tensor:
     return host
 
 
-def estimate_file(path, corr, chunk_sets: int = 64, taps_host: torch.Tensor | None = None) -> torch.Tensor:
+def estimate_file(path, corr, chunk_sets: int = 16, taps_host: torch.Tensor | None = None) -> torch.Tensor:
     """IQ file -> CSI taps in pinned host memory: the file is read in chunks of
     ``chunk_sets`` frame-sets into two pinned staging buffers while the previous chunk
     is copied to HBM, correlated and copied back (`Correlator.process_host`).  Returns
