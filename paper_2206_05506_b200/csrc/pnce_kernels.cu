@@ -256,6 +256,10 @@ struct CorrParams {
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
     int32_t store_hint;   // taps stores with an L2 evict_first policy (default; 0 via knob)
+    int32_t raw_pol;      // L2 policy of the raw f32 row loads: 0 evict_first, 1 normal, 2 evict_last
+    int32_t split_drain;  // release the first N half of a single accumulator early (see k_correlate)
+    int32_t truth_slots;  // scored drain: per-thread LDGSTS ring depth for the truth (0: register path)
+    uint32_t truth_off;   // byte offset of the truth ring in dynamic shared memory (after the raw ring)
     uint32_t stage_bytes;
     uint32_t tx_bytes;    // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
@@ -438,8 +442,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
 // current one is scaled and stored), then 16-column remainder pieces.
 template <bool SC>
 __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
-                                          float& s_abs, float& s_sq, float& nf) {
-    const int cols = p.g_cols;
+                                          float& s_abs, float& s_sq, float& nf, int cols) {
     int c = 0;
     LinkAcc la{-1, 0, 0.f};
     uint32_t va[32], vb[32];
@@ -539,8 +542,8 @@ __device__ __forceinline__ void epi_reps_scored(const CorrParams& p, const uint3
 }
 
 __device__ __forceinline__ void epi_block_scored(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
-                                                 float& s_abs, float& s_sq, float& nf) {
-    const int cols = p.g_cols;  // multiple of 32 here
+                                                 float& s_abs, float& s_sq, float& nf, int cols) {
+    // cols: multiple of 32 here
     const bool quad = (p.l & 7) == 0;
     LinkAcc la{-1, 0, 0.f};
     float4 h0[4], h1[4];
@@ -557,6 +560,51 @@ __device__ __forceinline__ void epi_block_scored(const CorrParams& p, uint32_t t
     };
     while (step(h0, h1) && step(h1, h0)) {
     }
+    if (p.link_err != nullptr) link_flush(p, e, la, quad);
+}
+
+// Scored drain with the truth staged through shared memory: each thread keeps a private
+// ring of D 32-column chunks (4 x 16 B per chunk: its two lags of every 8-lag repetition)
+// filled by LDGSTS, so D chunks of truth are in flight without holding registers -- the
+// register path above keeps one chunk in flight and is L2-latency bound.  Layout per warp:
+// [slot][rep][lane] x 16 B (conflict-free LDS.128).  Needs 16-byte aligned truth runs (even L).
+template <int D>
+__device__ __forceinline__ void epi_block_scored_smem(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
+                                                      uint32_t ring, float& s_abs, float& s_sq, float& nf,
+                                                      int cols) {
+    // cols: multiple of 32 here
+    const bool quad = (p.l & 7) == 0;
+    const int lane = threadIdx.x & 31;
+    LinkAcc la{-1, 0, 0.f};
+    auto issue = [&](int c, int slot) {
+        if (c < cols) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int lag = n0 + c + 8 * i;
+                const bool ok = e.out >= 0 && lag < e.n_valid;
+                const uint32_t bytes = ok ? (lag + 1 < e.n_valid ? 16u : 8u) : 0u;
+                const float* src = ok ? p.truth + 2 * (e.out + lag) : p.truth;
+                cp_async_16(ring + (uint32_t)(((slot * 4 + i) * 32 + lane) * 16), src, bytes);
+            }
+        }
+        cp_async_commit();  // (empty groups keep the in-order group count uniform)
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d) issue(32 * d, d);
+    uint32_t v[16];
+    float4 h[4];
+    int slot = 0;
+    for (int c = 0; c < cols; c += 32) {
+        tmem_ld_16x256b_x4(taddr + c, v);
+        cp_async_wait<D - 1>();  // chunk c's group has landed (groups retire in order)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = ld_shared_v4f(ring + (uint32_t)(((slot * 4 + i) * 32 + lane) * 16));
+        tmem_wait_ld();
+        epi_reps_scored(p, v, h, e, n0 + c, s_abs, s_sq, nf, la, quad);
+        issue(c + 32 * D, slot);  // refill the slot just consumed (its values are in registers)
+        if (++slot == D) slot = 0;
+    }
+    cp_async_wait<0>();
     if (p.link_err != nullptr) link_flush(p, e, la, quad);
 }
 
@@ -582,8 +630,7 @@ __device__ __forceinline__ void epi_reps_fast(const uint32_t* v, float* dst, flo
     }
 }
 
-__device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst) {
-    const int cols = p.g_cols;
+__device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst, int cols) {
     const float s = p.inv_m;
     const uint64_t pol = p.store_hint ? policy_evict_first() : 0ull;
     int c = 0;
@@ -692,7 +739,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
     // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
     // (packed/TMA mode has no converter work: EPI8 moves 4 of those warps to the epilogue)
-    constexpr int kCW = ((SCORED || EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
+    // (scored instantiations flip the flag: EPI8 = true there selects 8 converter + 4 epilogue warps)
+    constexpr int kCW = ((SCORED != EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
     constexpr int kEW0 = kConvWarp0 + kCW;
     constexpr int kEW = kWarps - kEW0;
     // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
@@ -754,12 +802,16 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
     const uint32_t a_bytes = kBM * kBK * 2;
     const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
+    // split drain (single accumulator of two N halves): the epilogue releases the first half
+    // early on tempty[1] and the MMA warp starts the next tile's first-half MMAs on it
+    const bool split = !T16 && p.split_drain && p.acc_stages == 1 && p.n_mma == 2;
 
 
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
-            const uint64_t pol_in = policy_evict_first();
+            const uint64_t pol_in = p.raw_pol == 0 ? policy_evict_first()
+                                                   : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
             const uint64_t pol_circ = policy_evict_last();
             int kb = 0, tile = cid, stage = 0;
             int mt = tile / p.n_groups, g = tile - mt * p.n_groups;
@@ -790,7 +842,74 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             PROF_END(0, 2);
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
+        if (leader && lane == 0 && split) {
+            // ===== MMA issuer, split-drain variant: per K-block the first-half MMAs (columns
+            // [0, nm)) go as soon as the epilogue released that half; second-half MMAs of the
+            // stages held meanwhile are issued once the whole accumulator is drained.
+            int stage = 0;
+            uint32_t phase = 0, tphase = 0;
+            int pend_stage0 = 0, pend_kb0 = 0;  // held stages are consecutive (ring order, kb order)
+            auto issue_half = [&](int st, int kb, int jj) {
+                const uint32_t sa = smem_u32(smem + (size_t)st * p.stage_bytes);
+                const uint32_t sb = sa + a_bytes;
+#pragma unroll
+                for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
+                    const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
+                    const uint64_t bd = make_sdesc(sb + jj * b_half_bytes + ks * 32, 16, 1024, 2);
+                    umma_f16_ss_pair(tmem_base + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kb | ks) != 0);
+                }
+            };
+            PROF_BEGIN(3);
+            for (int ti = 0; ti < my_tiles; ++ti) {
+                mbar_wait(&tempty[1], tphase ^ 1);
+                PROF_MARK(0);
+                TRACE(1, ti);
+                tc_fence_after();
+                bool hi_ok = false;
+                int np = 0;
+                auto flush = [&]() {
+                    tc_fence_after();
+                    hi_ok = true;
+                    int st = pend_stage0;
+                    for (int i = 0; i < np; ++i) {
+                        issue_half(st, pend_kb0 + i, 1);
+                        umma_commit_pair(&empty[st]);
+                        if (++st == S) st = 0;
+                    }
+                    np = 0;
+                };
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    if (!hi_ok && np == S) {  // every stage held: wait for the whole drain
+                        mbar_wait(&tempty[0], tphase ^ 1);
+                        flush();
+                    }
+                    mbar_wait(&full[stage], phase);
+                    PROF_MARK(1);
+                    TRACE(2, ti * p.k_blocks + kb);
+                    tc_fence_after();
+                    if (!hi_ok && mbar_test_wait(&tempty[0], tphase ^ 1)) flush();
+                    issue_half(stage, kb, 0);
+                    if (hi_ok) {
+                        issue_half(stage, kb, 1);
+                        umma_commit_pair(&empty[stage]);
+                    } else {
+                        if (np++ == 0) {
+                            pend_stage0 = stage;
+                            pend_kb0 = kb;
+                        }
+                    }
+                    if (++stage == S) { stage = 0; phase ^= 1u; }
+                    PROF_MARK(2);
+                }
+                if (!hi_ok) {
+                    mbar_wait(&tempty[0], tphase ^ 1);
+                    flush();
+                }
+                umma_commit_pair(&tfull[0]);
+                tphase ^= 1;
+            }
+            PROF_END(2, 3);
+        } else if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
             int acc = 0, stage = 0;
             uint32_t acc_phase = 0, phase = 0;
@@ -850,7 +969,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // ===== raw-chunk producer: TMA the f32 (I,Q) rows of this CTA's 64 links for half a
             // K-block (64 links x 32 samples x 8 B = 16 KB, +16 B per row when C is odd) into the
             // staging ring.  Finer chunks = more loads in flight for the same shared memory.
-            const uint64_t pol = policy_evict_first();
+            // evict_first when a row tile is read once; with several lag-row groups the
+            // neighbouring cluster reads the same rows for the next group (tiles are g-minor)
+            const uint64_t pol = p.raw_pol == 0 ? policy_evict_first()
+                                                : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
             int kb = 0, tile = cid, rs = 0;
             int mt = tile / p.n_groups;
             uint32_t rphase = 0;
@@ -1157,23 +1279,60 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 
             float s_abs[2] = {0.f, 0.f}, s_sq[2] = {0.f, 0.f}, nf[2] = {0.f, 0.f};
             const uint32_t t_acc = tmem_base + (uint32_t)(acc * p.g_cols);
+            if constexpr (SCORED) {
+                // split: as the plain drain below (per-link partials flush at the half boundary)
+                const int nh = split ? 2 : 1;
+                for (int h = 0; h < nh; ++h) {
+                    const int c0 = h ? p.nm : 0;
+                    const int nc = split ? (h ? p.g_cols - p.nm : p.nm) : p.g_cols;
 #pragma unroll
-            for (int k = 0; k < kBlocksPerWarp; ++k) {
-                const int bb = bb0 + k;
-                const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16);
-                if constexpr (SCORED) {
-                    const EpiLink e = make_link(p, link0 + 8 * bb);
-                    if (p.truth != nullptr && (p.g_cols & 31) == 0)
-                        epi_block_scored(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
-                    else
-                        epi_block<true>(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
-                } else {
-                    // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
-                    if (fast_dst[k] != nullptr) {
-                        epi_block_fast(p, taddr, fast_dst[k]);
-                    } else {
+                    for (int k = 0; k < kBlocksPerWarp; ++k) {
+                        const int bb = bb0 + k;
+                        const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16) + (uint32_t)c0;
                         const EpiLink e = make_link(p, link0 + 8 * bb);
-                        epi_block<false>(p, taddr, e, n0, s_abs[k], s_sq[k], nf[k]);
+                        const uint32_t ring =
+                            smem_u32(smem) + p.truth_off + (uint32_t)((warp - kEW0) * p.truth_slots * 2048);
+                        const bool c32 = p.truth != nullptr && (nc & 31) == 0;
+                        if (p.truth_slots == 2 && c32)
+                            epi_block_scored_smem<2>(p, taddr, e, n0 + c0, ring, s_abs[k], s_sq[k], nf[k], nc);
+                        else if (p.truth_slots == 3 && c32)
+                            epi_block_scored_smem<3>(p, taddr, e, n0 + c0, ring, s_abs[k], s_sq[k], nf[k], nc);
+                        else if (p.truth_slots == 4 && c32)
+                            epi_block_scored_smem<4>(p, taddr, e, n0 + c0, ring, s_abs[k], s_sq[k], nf[k], nc);
+                        else if (c32)
+                            epi_block_scored(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
+                        else
+                            epi_block<true>(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
+                    }
+                    if (split && h == 0) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + 8u);
+                    }
+                }
+            } else {
+                // plain drain; split: columns [0, nm) of every block first, released to the MMA
+                // warp (the next tile's first-half MMAs) before [nm, g_cols) is drained
+                const int nh = split ? 2 : 1;
+                for (int h = 0; h < nh; ++h) {
+                    const int c0 = h ? p.nm : 0;
+                    const int nc = split ? (h ? p.g_cols - p.nm : p.nm) : p.g_cols;
+#pragma unroll
+                    for (int k = 0; k < kBlocksPerWarp; ++k) {
+                        const int bb = bb0 + k;
+                        const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16) + (uint32_t)c0;
+                        // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
+                        if (fast_dst[k] != nullptr) {
+                            epi_block_fast(p, taddr, fast_dst[k] + 2 * c0, nc);
+                        } else {
+                            const EpiLink e = make_link(p, link0 + 8 * bb);
+                            epi_block<false>(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
+                        }
+                    }
+                    if (split && h == 0) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + 8u);
                     }
                 }
             }
@@ -1398,6 +1557,9 @@ static cudaError_t set_smem_attrs() {
     if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
         e = cudaFuncSetAttribute(k_correlate<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemLimit);
+    if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
+        e = cudaFuncSetAttribute(k_correlate<MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemLimit);
     if (e == cudaSuccess && MODE == kModeFusedTma)
         e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -1416,7 +1578,14 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
         return e ? std::atoi(e) : -1;
     }();
     const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
-    if (scored)
+    // scored: 4 converter + 8 epilogue warps by default; PNCE_TUNE_SCORED_CONV8=1 -> 8 + 4
+    static const bool sc_conv8 = [] {
+        const char* e = std::getenv("PNCE_TUNE_SCORED_CONV8");
+        return e && std::atoi(e) == 1;
+    }();
+    if (scored && sc_conv8 && (MODE == kModeFusedTma || MODE == kModePacked))
+        k_correlate<MODE, true, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+    else if (scored)
         k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
     else if ((MODE == kModeFusedTma || MODE == kModePacked) && epi8)
         k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
@@ -1707,6 +1876,13 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     const char* sh = std::getenv("PNCE_TUNE_STORE_HINT");
     prm.store_hint = sh ? std::atoi(sh) : 1;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
     prm.n_groups = t.n_groups;
+    const char* rp = std::getenv("PNCE_TUNE_RAW_POL");
+    prm.raw_pol = rp ? std::atoi(rp) : (t.n_groups > 1 ? 1 : 0);
+    static const int split_env = [] {
+        const char* e = std::getenv("PNCE_TUNE_SPLIT_DRAIN");
+        return e ? std::atoi(e) : 1;
+    }();
+    prm.split_drain = split_env;
     prm.g_cols = t.g_cols;
     prm.n_mma = t.n_mma;
     prm.nm = t.nm;
@@ -1898,7 +2074,18 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         // rest of shared memory as the raw half-K-block ring (its depth hides HBM latency:
         // ~1.3 us per load vs ~0.4 us of MMA per chunk)
         prm.raw_stage_bytes = (uint32_t)(kLinksPerTile * prm.raw_row_floats * 4);
-        const int64_t budget = (int64_t)kSmemLimit - 2048;
+        int64_t budget = (int64_t)kSmemLimit - 2048;
+        // scored drain: truth staged through a per-thread LDGSTS ring (8 epilogue warps x
+        // slots x 2 KB) when the truth runs are 16-byte aligned (PNCE_TUNE_TRUTH_SLOTS, 0 = off)
+        static const int truth_slots_env = [] {
+            const char* e = std::getenv("PNCE_TUNE_TRUTH_SLOTS");
+            return e ? std::atoi(e) : 3;
+        }();
+        if (scored && truth && (p->cfg.l % 2) == 0 && (reinterpret_cast<uintptr_t>(truth) & 15) == 0 &&
+            (prm.g_cols & 31) == 0 && truth_slots_env >= 2 && truth_slots_env <= 4) {
+            prm.truth_slots = truth_slots_env;
+            budget -= (int64_t)8 * prm.truth_slots * 2048;
+        }
         int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
         const char* as = std::getenv("PNCE_TUNE_AB_STAGES");
         if (as) ab = std::min<int>((int)(budget / prm.stage_bytes), std::max(1, std::atoi(as)));
@@ -1908,8 +2095,9 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
         prm.raw_stages = raw;
-        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024 +
-                            (size_t)prm.raw_stages * prm.raw_stage_bytes;
+        prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + 1024 +
+                                   (size_t)prm.raw_stages * prm.raw_stage_bytes);
+        const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)8 * prm.truth_slots * 2048;
         if (t16) {
             const int64_t n_fb = n_frames * p->n_batches;
             uint32_t* flags = nullptr;
