@@ -257,6 +257,11 @@ struct CorrParams {
     uint32_t raw_stage_bytes;
     int32_t store_hint;   // taps stores with an L2 evict_first policy (default; 0 via knob)
     int32_t raw_pol;      // L2 policy of the raw f32 row loads: 0 evict_first, 1 normal, 2 evict_last
+    int32_t a_reuse;      // FusedTma, n_groups > 1: group 0 converts once and stores the fp16 A
+                          // stages to `scratch`; the other groups of the row tile TMA them back
+    uint32_t bar_bytes;   // barrier block bytes (1 KB; 2 KB with a_reuse: + scratch barriers)
+    int32_t scr_pol;      // a_reuse: 1 = evict_last L2 policy on the scratch stores / reloads
+    uint8_t* scratch;     // a_reuse: [2 slots][clusters][2 CTAs][k_blocks][128 rows][128 B]
     int32_t split_drain;  // release the first N half of a single accumulator early (see k_correlate)
     int32_t truth_slots;  // scored drain: per-thread LDGSTS ring depth for the truth (0: register path)
     uint32_t truth_off;   // byte offset of the truth ring in dynamic shared memory (after the raw ring)
@@ -731,7 +736,7 @@ __device__ __forceinline__ void t16_fold(const CorrParams& p, uint32_t t_part, u
 template <int MODE, bool SCORED, bool EPI8 = false, bool T16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
-            const CorrParams p) {
+            const __grid_constant__ CUtensorMap tm_scr, const CorrParams p) {
     constexpr bool A_TMA = MODE == kModePacked;     // A via TMA with the circulant
     constexpr bool RAW = MODE == kModeFusedTma;     // f32 rows TMA-staged, converted
     constexpr bool FLDG = MODE == kModeFusedLdg;    // f32 rows LDG'd, converted
@@ -758,7 +763,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     uint64_t* raw_full = tempty + 2;
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
-    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
+    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + p.bar_bytes;
+    // a_reuse: per (slot, K-block) "A stage stored" barriers in the second KB of the block
+    uint64_t* scr_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes + 1024);
+    const bool reuse = RAW && p.a_reuse;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -783,11 +791,14 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 mbar_init(&raw_empty[s], kCW);
             }
         }
+        if (reuse)
+            for (int s = 0; s < 2 * p.k_blocks; ++s) mbar_init(&scr_full[s], 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         if (A_TMA || RAW) tma_prefetch(&tm_in);
         tma_prefetch(&tm_circ);
+        if (reuse) tma_prefetch(&tm_scr);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
     tc_fence_before();
@@ -798,7 +809,24 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int n_clusters = gridDim.x >> 1;
     const int cid = blockIdx.x >> 1;
     const int total_tiles = p.m_tiles * p.n_groups;
-    const int my_tiles = cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0;
+    // Tile order: tile = cid + ti * n_clusters, (row tile, group) = divmod(tile, n_groups);
+    // with a_reuse a cluster takes whole row tiles (all groups back to back, group 0 first).
+    const int my_rows = cid < p.m_tiles ? (p.m_tiles - 1 - cid) / n_clusters + 1 : 0;
+    const int my_tiles = reuse ? my_rows * p.n_groups
+                               : (cid < total_tiles ? (total_tiles - 1 - cid) / n_clusters + 1 : 0);
+    auto coords = [&](int ti) -> int2 {  // (row tile, group)
+        if (reuse) {
+            const int r = ti / p.n_groups;
+            return make_int2(cid + r * n_clusters, ti - r * p.n_groups);
+        }
+        const int tile = cid + ti * n_clusters;
+        const int mt = tile / p.n_groups;
+        return make_int2(mt, tile - mt * p.n_groups);
+    };
+    // scratch row of (row-tile iteration r, this CTA, K-block kb); slots alternate per row tile
+    auto scr_row = [&](int r, int kb) -> int {
+        return ((((r & 1) * n_clusters + cid) * 2 + (int)rank) * p.k_blocks + kb) * kBM;
+    };
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
     const uint32_t a_bytes = kBM * kBK * 2;
     const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
@@ -813,8 +841,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const uint64_t pol_in = p.raw_pol == 0 ? policy_evict_first()
                                                    : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
             const uint64_t pol_circ = policy_evict_last();
-            int kb = 0, tile = cid, stage = 0;
-            int mt = tile / p.n_groups, g = tile - mt * p.n_groups;
+            int kb = 0, ti = 0, stage = 0, mt = 0, g = 0;
+            { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
             uint32_t phase = 0;
             PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
@@ -824,18 +852,27 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
                 uint8_t* sb = sa + a_bytes;
                 const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
-                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
+                const bool from_scr = reuse && g > 0;
+                const int r = ti / p.n_groups;
+                if (from_scr) {
+                    // group 0 of this row tile stored the converted A stage of K-block kb
+                    mbar_wait(&scr_full[(r & 1) * p.k_blocks + kb], (uint32_t)(r >> 1) & 1u);
+                    fence_proxy_async_global();
+                }
+                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes + (from_scr ? 2 * a_bytes : 0u));
                 if (A_TMA)
                     tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
+                if (from_scr)  // keep the stage in L2 for the row tile's later groups
+                    tma_load_2d_pair(sa, &tm_scr, fb_leader, 0, scr_row(r, kb),
+                                     g == p.n_groups - 1 ? policy_evict_first()
+                                                         : (p.scr_pol ? policy_evict_last() : policy_evict_normal()));
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
                                      g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
                 if (++kb == p.k_blocks) {
                     kb = 0;
-                    tile += n_clusters;
-                    mt = tile / p.n_groups;
-                    g = tile - mt * p.n_groups;
+                    { const int2 _c = coords(++ti); mt = _c.x; g = _c.y; }
                 }
                 PROF_MARK(1);
             }
@@ -973,13 +1010,14 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // neighbouring cluster reads the same rows for the next group (tiles are g-minor)
             const uint64_t pol = p.raw_pol == 0 ? policy_evict_first()
                                                 : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
-            int kb = 0, tile = cid, rs = 0;
-            int mt = tile / p.n_groups;
+            int kb = 0, ti = 0, rs = 0, mt = 0, g = 0;
+            { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
             uint32_t rphase = 0;
             PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
+                // a_reuse: only group 0 reads the raw rows
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 2 && !(reuse && g > 0); ++h) {
                     mbar_wait(&raw_empty[rs], rphase ^ 1u);
                     PROF_MARK(0);
                     if (h == 0) TRACE(6, j);
@@ -998,8 +1036,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
                 if (++kb == p.k_blocks) {
                     kb = 0;
-                    tile += n_clusters;
-                    mt = tile / p.n_groups;
+                    { const int2 _c = coords(++ti); mt = _c.x; g = _c.y; }
                 }
             }
             PROF_END(5, 2);
@@ -1007,11 +1044,18 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     } else if (warp >= kConvWarp0 && warp < kEW0) {
         if (RAW) {
             const int cw = warp - kConvWarp0;
-            int kb = 0, stage = 0, rs = 0;
+            int kb = 0, stage = 0, rs = 0, ti = 0, mt = 0, g = 0;
+            { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
             uint32_t phase = 0, rphase = 0;
             PROF_BEGIN(3);
             for (int j = 0; j < jobs; ++j) {
                 const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                if (reuse && g > 0) {
+                    // the A stage comes from the scratch by TMA: only keep the arrival count
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
+                } else {
                     // staged f32 chunks -> A stage.  Per chunk a warp converts 8 links: lanes
                     // 0-15 link a, lanes 16-31 link a+4 (so the two Re rows fall in different
                     // swizzle halves: conflict-free STS); lane l handles samples 2(l%16), +1
@@ -1066,10 +1110,43 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                         if (cw == 0) TRACE(9, j);
                     }
+                    if (reuse) {
+                        // group 0: store the converted A stage (16 KB, swizzled image) to the
+                        // scratch for the row tile's other groups once every converter warp has
+                        // fenced its STS.  The issuer first waits for the previous store's smem
+                        // reads (issued a job ago: that stage is rewritten after this barrier
+                        // when S = 2); a K-block's barrier fires once its store has completed,
+                        // kScrLag stores later (all of them at the row tile's last K-block).
+                        constexpr int kScrLag = 4;
+                        if (cw == 0 && lane == 0) bulk_wait_read<0>();
+                        named_bar_sync(1, kCW * 32);
+                        if (cw == 0 && lane == 0) {
+                            const int r = ti / p.n_groups;
+                            if (p.scr_pol)
+                                bulk_store_s2g_hint(p.scratch + (size_t)scr_row(r, kb) * 128, sa, a_bytes,
+                                                    policy_evict_last());
+                            else
+                                bulk_store_s2g(p.scratch + (size_t)scr_row(r, kb) * 128, sa, a_bytes);
+                            bulk_commit();
+                            uint64_t* sf = &scr_full[(r & 1) * p.k_blocks];
+                            if (kb == p.k_blocks - 1) {
+                                bulk_wait<0>();
+                                for (int q = max(0, kb - kScrLag); q <= kb; ++q) mbar_arrive(&sf[q]);
+                            } else if (kb >= kScrLag) {
+                                bulk_wait<kScrLag>();
+                                mbar_arrive(&sf[kb - kScrLag]);
+                            }
+                        }
+                    }
+                }
                 PROF_MARK(2);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
-                if (++kb == p.k_blocks) kb = 0;
+                if (++kb == p.k_blocks) {
+                    kb = 0;
+                    { const int2 _c = coords(++ti); mt = _c.x; g = _c.y; }
+                }
             }
+            if (reuse && cw == 0 && lane == 0) bulk_wait<0>();  // shared memory must outlive the stores
             if (cw == 0 && lane == 0) PROF_END(7, 3);
         } else if (FLDG) {
             // ===== pipelined LDG converters.  Group gsel (warps 4-7 / 8-11) converts the jobs
@@ -1207,9 +1284,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // total at [G, 2G) (single-buffered: the MMA waits for each fold)
             const int n_units = (p.k_blocks + p.chunk_kb - 1) / p.chunk_kb;
             for (int ti = 0; ti < my_tiles; ++ti) {
-                const int tile = cid + ti * n_clusters;
-                const int mt = tile / p.n_groups;
-                const int g = tile - mt * p.n_groups;
+                int mt, g;
+                { const int2 _c = coords(ti); mt = _c.x; g = _c.y; }
                 const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
                 const int n0 = g * p.g_cols + colp;
                 bool sat[2] = {false, false};
@@ -1237,9 +1313,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             }
         } else
         for (int ti = 0; ti < my_tiles; ++ti) {
-            const int tile = cid + ti * n_clusters;
-            const int mt = tile / p.n_groups;
-            const int g = tile - mt * p.n_groups;
+            int mt, g;
+            { const int2 _c = coords(ti); mt = _c.x; g = _c.y; }
             const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
             // (links are re-derived where needed instead of kept live: register pressure)
             const int n0 = g * p.g_cols + colp;
@@ -1488,6 +1563,22 @@ pnce_status_t make_tmap_raw(CUtensorMap* map, const float* base, uint64_t row_fl
     return PNCE_OK;
 }
 
+// A-stage scratch (a_reuse) as a 2-D tensor [rows][128 B] of 16-bit words, box [128 rows][64],
+// no swizzle: the stored bytes are already the 128B-swizzled shared-memory image of a stage.
+pnce_status_t make_tmap_scr(CUtensorMap* map, const void* base, uint64_t rows) {
+    auto enc = get_encode();
+    if (!enc) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)kBK, rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kBK * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PNCE_ERR_CUDA, "cuTensorMapEncodeTiled(scratch) failed: " + std::to_string((int)r));
+    return PNCE_OK;
+}
+
 }  // namespace
 
 // Lag-row tiling of one K3 variant.
@@ -1570,7 +1661,8 @@ static cudaError_t set_smem_attrs() {
 // plain drain keeps its registers.
 template <int MODE>
 static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
-                      const CUtensorMap& b, const CorrParams& prm) {
+                      const CUtensorMap& b, const CorrParams& prm, const CUtensorMap* scr = nullptr) {
+    const CUtensorMap& c = scr ? *scr : b;  // scratch map (a_reuse) or an unused placeholder
     // 8 epilogue warps: +1 % for the packed operand (its converter warps are idle anyway),
     // -5 % for the fused path (converters become the bottleneck); PNCE_TUNE_EPI8 overrides
     static const int epi8_env = [] {
@@ -1584,13 +1676,13 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
         return e && std::atoi(e) == 1;
     }();
     if (scored && sc_conv8 && (MODE == kModeFusedTma || MODE == kModePacked))
-        k_correlate<MODE, true, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+        k_correlate<MODE, true, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else if (scored)
-        k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+        k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else if ((MODE == kModeFusedTma || MODE == kModePacked) && epi8)
-        k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+        k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else
-        k_correlate<MODE, false><<<grid, kThreadsK3, smem, st>>>(a, b, prm);
+        k_correlate<MODE, false><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
 }
 
 // Tilings, operand rows and tensor maps of a plan: the PN lag-window rows built from the
@@ -1876,6 +1968,7 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     const char* sh = std::getenv("PNCE_TUNE_STORE_HINT");
     prm.store_hint = sh ? std::atoi(sh) : 1;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
     prm.n_groups = t.n_groups;
+    prm.bar_bytes = 1024;
     const char* rp = std::getenv("PNCE_TUNE_RAW_POL");
     prm.raw_pol = rp ? std::atoi(rp) : (t.n_groups > 1 ? 1 : 0);
     static const int split_env = [] {
@@ -2075,6 +2168,19 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         // ~1.3 us per load vs ~0.4 us of MMA per chunk)
         prm.raw_stage_bytes = (uint32_t)(kLinksPerTile * prm.raw_row_floats * 4);
         int64_t budget = (int64_t)kSmemLimit - 2048;
+        // a_reuse (several lag-row groups): convert a row tile once, keep its fp16 A stages in an
+        // L2-resident scratch for the other groups (PNCE_TUNE_A_REUSE=0: convert per group)
+        static const int reuse_env = [] {
+            const char* e = std::getenv("PNCE_TUNE_A_REUSE");
+            return e ? std::atoi(e) : 1;
+        }();
+        if (reuse_env == 1 && tiling.n_groups > 1 && prm.k_blocks <= 64) {
+            prm.a_reuse = 1;
+            const char* sp = std::getenv("PNCE_TUNE_SCR_POL");
+            prm.scr_pol = sp ? std::atoi(sp) : 1;
+            prm.bar_bytes = 2048;
+            budget -= 1024;
+        }
         // scored drain: truth staged through a per-thread LDGSTS ring (8 epilogue warps x
         // slots x 2 KB) when the truth runs are 16-byte aligned (PNCE_TUNE_TRUTH_SLOTS, 0 = off)
         static const int truth_slots_env = [] {
@@ -2095,9 +2201,34 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
         prm.raw_stages = raw;
-        prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + 1024 +
+        prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + prm.bar_bytes +
                                    (size_t)prm.raw_stages * prm.raw_stage_bytes);
         const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)8 * prm.truth_slots * 2048;
+        const int grid = pair_grid(p, prm);
+        CUtensorMap tm_scr;
+        void* scratch = nullptr;
+        if (prm.a_reuse) {
+            // [2 slots][clusters][2 CTAs][k_blocks] A stages of 128 rows x 128 B (stream-ordered
+            // allocation: the pool keeps it, so repeated launches do not reach the driver)
+            static std::once_flag pool_once;
+            std::call_once(pool_once, [] {
+                int dev = 0;
+                cudaMemPool_t pool;
+                if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t keep = UINT64_MAX;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                }
+            });
+            const uint64_t rows = (uint64_t)2 * (grid / 2) * 2 * prm.k_blocks * kBM;
+            cudaError_t e = cudaMallocAsync(&scratch, rows * 128, st);
+            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("A scratch: ") + cudaGetErrorString(e));
+            prm.scratch = static_cast<uint8_t*>(scratch);
+            s = make_tmap_scr(&tm_scr, scratch, rows);
+            if (s != PNCE_OK) {
+                cudaFreeAsync(scratch, st);
+                return s;
+            }
+        }
         if (t16) {
             const int64_t n_fb = n_frames * p->n_batches;
             uint32_t* flags = nullptr;
@@ -2108,8 +2239,8 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.acc16 = t16->acc16;
             prm.sat_flags = flags;
             if (t16->acc16) prm.idesc &= ~(3u << 4);  // c_format = F16: binary16 partials in TMEM
-            k_correlate<kModeFusedTma, false, false, true><<<pair_grid(p, prm), kThreadsK3, smem, st>>>(
-                tm_raw, p->t16.tm_circ, prm);
+            k_correlate<kModeFusedTma, false, false, true><<<grid, kThreadsK3, smem, st>>>(
+                tm_raw, p->t16.tm_circ, prm.a_reuse ? tm_scr : p->t16.tm_circ, prm);
             g_launches++;
             const pnce_cfg_t& c = p->cfg;
             k_t16_finish<<<(unsigned)n_fb, 256, 0, st>>>(taps, truth, stats, flags, c.n_r, c.n_t, c.n_batch,
@@ -2118,8 +2249,10 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             cudaFreeAsync(flags, st);
             if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16: ") + cudaGetErrorString(e));
         } else {
-            launch_k3<kModeFusedTma>(scored, pair_grid(p, prm), smem, st, tm_raw, tiling.tm_circ, prm);
+            launch_k3<kModeFusedTma>(scored, grid, smem, st, tm_raw, tiling.tm_circ, prm,
+                                     prm.a_reuse ? &tm_scr : nullptr);
         }
+        if (scratch) cudaFreeAsync(scratch, st);
     } else {
         if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
