@@ -212,6 +212,43 @@ def ingest_leg(corr, iq, taps, w, Ff, rank):
             "timing": "host wall clock, file in page cache"}
 
 
+def cfg4_leg(P, S, dev, stream, F4, steps, tf_burst, tf_sust):
+    """BASELINE configs[3] (cfg4': 128x128 MIMO, PN 2047, L=C=127, N_b=16 -> 2032 lag rows,
+    four 512-column groups): the tensor-bound configuration.  Fused kernel (f32 IQ in) and
+    the GEMM on the pre-packed fp16 operand, device-synthesised inputs, CUDA events."""
+    import torch
+    cfg = P.PilotConfig(m=2047, c=127, n_t=128, n_batch=16, l=127, f_s=10e6)
+    corr = P.Correlator(P.default_spec(11), cfg, 128, device=dev)
+    h = S.draw_channel(corr, F4, seed=77)
+    iq = S.simulate_frames(corr, h, 10.0, seed=78)
+    del h
+    taps = torch.empty(corr.taps_shape(F4), dtype=torch.complex64, device=dev)
+    flop = 4.0 * cfg.n_t * cfg.l * cfg.m * 128
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / 1e3 / steps / F4
+
+    tf = timed(lambda: corr.process(iq, out=taps))
+    packed = corr.pack(iq)
+    tp = timed(lambda: corr.correlate(packed, F4, out=taps))
+    del packed, iq, taps
+    out = {"workload": "cfg4' 128x128 MIMO, PN 2047, L=C=127, N_batch=16 (BASELINE configs[3])", "frames": F4,
+           "flop_per_frame": flop}
+    for name, t in (("fused", tf), ("gemm", tp)):
+        out[name] = {"us_per_frame": t * 1e6, "tflops": flop / t / 1e12, "frac_of_bf16_peak": flop / t / 1e12 / tf_burst,
+                     "frac_of_bf16_sustained": (flop / t / 1e12 / tf_sust) if tf_sust else None}
+    return out
+
+
 def run_gpu(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -367,6 +404,11 @@ def run_gpu(args, rank, world):
                 "gbs": bytes_gemm_f * Fg / tg / 1e9}
         del packed
 
+    # --- BASELINE configs[3] (cfg4', tensor-bound): fused and packed-GEMM tensor fractions
+    c4 = None
+    if args.cfg4_frames > 0:
+        c4 = cfg4_leg(P, S, dev, stream, args.cfg4_frames, args.steps, tf_burst, tf_sust)
+
     # --- e2e through the public API with pinned host buffers (H2D in, D2H taps out)
     e2e = None
     if not args.no_e2e:
@@ -440,6 +482,7 @@ def run_gpu(args, rank, world):
             "gemm_leg": gemm,
             "estimate_quality": quality,
             "tensor16_leg": t16,
+            "cfg4_leg": c4,
             "cpu_baseline": cpu, "e2e": e2e, "ingest_iq_file": ingest, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -463,6 +506,7 @@ def main():
     ap.add_argument("--no-quality", action="store_true", help="skip the fused-scoring quality pass")
     ap.add_argument("--scored-frames", type=int, default=2048, help="frame-sets in the fused-scoring pass")
     ap.add_argument("--gemm-frames", type=int, default=4096)
+    ap.add_argument("--cfg4-frames", type=int, default=256, help="frame-sets in the cfg4' leg (0: off)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
