@@ -1468,274 +1468,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     }
 }
 
-// ------------------------------------------------------------------ K3 quad
-// Fused correlation on a 4-CTA cluster = two CTA pairs working on the SAME 128-link row tile:
-// pair p (ranks 2p, 2p+1) computes lag group p (<= 256 columns), so each pair's accumulator
-// is double-buffered in TMEM (2 x 256 columns) and a tile's drain overlaps the next tile's
-// MMAs -- which a single pair cannot do at R = 512 (the accumulator fills TMEM).  The
-// samples are converted once per row tile: CTA (p, q) converts 32 of the 64 links of
-// half q (links 32p..32p+31) from its own raw staging ring into rows 64p..64p+63 of its
-// A stage and bulk-copies those 8 KB into the same rows of the partner CTA (p^1, q) over
-// DSMEM (cp.async.bulk shared::cta -> shared::cluster, completion on the partner's barrier;
-// a peer CTA's copy lands on its `xfull` barrier and warp 3 forwards it to the pair leader).
-// Per unit of MMA work the TMA ingress (raw + circulant) equals the pair kernel's.
-// Stage release counts both pairs' MMA commits (multicast to all four CTAs), since every
-// A stage is written by converters of two pairs.
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsK3, 1)
-k_correlate_quad(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
-                 const CorrParams p) {
-    constexpr int kCW = kConvWarps;            // 8 converter warps (4..11), 4 epilogue warps (12..15)
-    constexpr int kEW0 = kConvWarp0 + kCW;
-    constexpr int kEW = kWarps - kEW0;
-    constexpr int kHalfLinks = kLinksPerTile / 2;  // 32 links converted per CTA
-    constexpr uint32_t kHalfA = kBM * kBK;          // bytes of 64 A rows (32 links) = 8 KB
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int S = p.stages;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
-    uint64_t* empty = full + S;
-    uint64_t* xfull = empty + S;
-    uint64_t* tfull = xfull + S;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* raw_full = tempty + 2;
-    uint64_t* raw_empty = raw_full + p.raw_stages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + p.raw_stages);
-    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + 1024;
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
-    const int pair = (int)(rank >> 1);
-    const uint32_t q = rank & 1u;  // 0: pair leader (A rows 0..127 = links 0..63 of the tile)
-    const uint32_t lrank = rank & ~1u, partner = rank ^ 2u;
-    const bool leader = q == 0;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            // leader: producer expect_tx (circulant of both CTAs + the partner's 8 KB copy) +
-            // converter warps of both CTAs of the pair + the peer's copy forwarder
-            mbar_init(&full[s], 1 + 2 * kCW + 1);
-            mbar_init(&empty[s], 2);  // MMA commits of both pairs
-            mbar_init(&xfull[s], 1);  // peer CTAs: the partner's copy (forwarder's expect_tx)
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * kEW);
-        }
-        for (int s = 0; s < p.raw_stages; ++s) {
-            mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], kCW);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0 && lane == 0) {
-        tma_prefetch(&tm_in);
-        tma_prefetch(&tm_circ);
-    }
-    if (warp == 1) tmem_alloc_pair(tmem_slot, p.tmem_cols);
-    tc_fence_before();
-    cluster_sync_all();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    const int n_quads = gridDim.x >> 2;
-    const int qid = blockIdx.x >> 2;
-    const int my_tiles = qid < p.m_tiles ? (p.m_tiles - 1 - qid) / n_quads + 1 : 0;
-    const int jobs = my_tiles * p.k_blocks;
-    const uint32_t a_bytes = kBM * kBK * 2;
-    const uint32_t b_half_bytes = (uint32_t)(p.nm / 2) * kBK * 2;
-    const int g = pair;  // lag group of this pair
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ===== circulant producer (this pair's lag group, this CTA's half of the rows)
-            const uint64_t pol_circ = policy_evict_last();
-            int kb = 0, stage = 0;
-            uint32_t phase = 0;
-            for (int j = 0; j < jobs; ++j) {
-                mbar_wait(&empty[stage], phase ^ 1u);
-                uint8_t* sb = smem + (size_t)stage * p.stage_bytes + a_bytes;
-                const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), lrank);
-#ifdef PNCE_DIAG_QUAD_NOCOPY
-                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-#else
-                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes + kHalfA);
-#endif
-                tma_load_2d_pair(sb, &tm_circ, fb_leader, kb * kBK, g * p.g_cols + (int)q * (p.nm / 2), pol_circ);
-                if (++stage == S) { stage = 0; phase ^= 1u; }
-                if (++kb == p.k_blocks) kb = 0;
-            }
-        }
-    } else if (warp == 1) {
-        if (leader && lane == 0) {
-            // ===== MMA issuer of this pair: double-buffered accumulators of g_cols columns
-            int acc = 0, stage = 0;
-            uint32_t acc_phase = 0, phase = 0;
-            const uint16_t pair_mask = (uint16_t)(3u << (2 * pair));
-            for (int ti = 0; ti < my_tiles; ++ti) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
-                    const uint32_t sb = sa + a_bytes;
-#pragma unroll
-                    for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
-                        const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
-                        const uint64_t bd = make_sdesc(sb + ks * 32, 16, 1024, 2);
-                        umma_f16_ss_pair(d_tmem, ad, bd, p.idesc, (kb | ks) != 0);
-                    }
-                    umma_commit_pair_mc(&empty[stage], (uint16_t)0xF);  // both pairs' converters wait on it
-                    if (++stage == S) { stage = 0; phase ^= 1u; }
-                }
-                umma_commit_pair_mc(&tfull[acc], pair_mask);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            }
-        }
-    } else if (warp == 2) {
-        if (lane == 0) {
-            // ===== raw producer: this CTA's 32 links, half-K-block chunks (32 links x 32 samples)
-            const uint64_t pol = policy_evict_first();
-            int kb = 0, ti = 0, rs = 0;
-            uint32_t rphase = 0;
-            for (int j = 0; j < jobs; ++j) {
-                const int mt = qid + ti * n_quads;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    mbar_wait(&raw_empty[rs], rphase ^ 1u);
-                    mbar_arrive_expect_tx(&raw_full[rs], p.raw_stage_bytes);
-                    tma_load_2d(raw_base + (size_t)rs * p.raw_stage_bytes, &tm_in, &raw_full[rs],
-                                (2 * (p.c + kb * kBK + h * kRawChunk)) & ~3,
-                                (mt * 2 + (int)q) * kLinksPerTile + pair * kHalfLinks, pol);
-                    if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
-                }
-                if (++kb == p.k_blocks) { kb = 0; ++ti; }
-            }
-        }
-    } else if (warp == 3) {
-        if (!leader && lane == 0) {
-            // ===== peer CTAs: forward the partner's DSMEM copy (landed on xfull) to the leader
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int j = 0; j < jobs; ++j) {
-#ifndef PNCE_DIAG_QUAD_NOCOPY
-                mbar_arrive_expect_tx(&xfull[stage], kHalfA);
-                mbar_wait(&xfull[stage], phase);
-#else
-                mbar_wait(&empty[stage], phase ^ 1u);
-#endif
-                mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), lrank));
-                if (++stage == S) { stage = 0; phase ^= 1u; }
-            }
-        }
-    } else if (warp < kEW0) {
-        // ===== converters: 32 links per job into A rows 64*pair.., then the 8 KB DSMEM copy
-        const int cw = warp - kConvWarp0;
-        int kb = 0, stage = 0, rs = 0;
-        uint32_t phase = 0, rphase = 0;
-        for (int j = 0; j < jobs; ++j) {
-            uint8_t* sa_ptr = smem + (size_t)stage * p.stage_bytes;
-            const uint32_t sa = smem_u32(sa_ptr);
-            mbar_wait(&empty[stage], phase ^ 1u);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                mbar_wait(&raw_full[rs], rphase);
-                const int slack = (2 * (p.c + kb * kBK + h * kRawChunk)) & 3;
-                const uint32_t raw = smem_u32(raw_base + (size_t)rs * p.raw_stage_bytes) + slack * 4 + (lane & 15) * 16;
-                const int k = kb * kBK + h * kRawChunk + 2 * (lane & 15);
-                const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
-                const int col_byte = h * 64 + (lane & 15) * 4;
-#pragma unroll
-                for (int it = 0; it < kHalfLinks / (2 * kCW); ++it) {
-                    const int idx = cw + kCW * it;  // 0..15
-                    const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);  // 0..31
-                    const uint32_t src = raw + link * (p.raw_row_floats * 4);
-                    float4 v;
-                    if (slack == 0) {
-                        v = ld_shared_v4f(src);
-                    } else {
-                        const float2 a = ld_shared_v2f(src);
-                        const float2 b = ld_shared_v2f(src + 8);
-                        v = make_float4(a.x, a.y, b.x, b.y);
-                    }
-                    if (!ok0) { v.x = 0.f; v.y = 0.f; }
-                    if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                    const int tl = pair * kHalfLinks + link;  // link within this CTA's 64
-                    st_shared_u32(swz(sa, (int)a_row(tl, 0), col_byte), pack2(v.x, v.z, p.bf16));
-                    st_shared_u32(swz(sa, (int)a_row(tl, 1), col_byte), pack2(v.y, v.w, p.bf16));
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&raw_empty[rs]);
-                if (++rs == p.raw_stages) { rs = 0; rphase ^= 1u; }
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), lrank));
-            // all converter warps fenced -> copy the 8 KB half into the partner CTA's stage
-#ifndef PNCE_DIAG_QUAD_NOCOPY
-            named_bar_sync(1, kCW * 32);
-            if (cw == 0 && lane == 0) {
-#else
-            if (false) {
-#endif
-                const uint32_t off = (uint32_t)pair * kHalfA;
-                uint64_t* bar = leader ? &full[stage] : &xfull[stage];
-                bulk_copy_s2s(mapa_shared(sa + off, partner), sa_ptr + off, kHalfA,
-                              mapa_shared(smem_u32(bar), partner));
-            }
-            if (++stage == S) { stage = 0; phase ^= 1u; }
-            if (++kb == p.k_blocks) kb = 0;
-        }
-    } else {
-        // ===== epilogue: this pair's lag group, double-buffered accumulator
-        const int quarter = warp & 3;
-        const int colp = 2 * (lane & 3);
-        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), lrank);
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int ti = 0; ti < my_tiles; ++ti) {
-            const int mt = qid + ti * n_quads;
-            const int64_t link0 = ((int64_t)mt * 2 + q) * kLinksPerTile + quarter * 16 + (lane >> 2);
-            const int n0 = g * p.g_cols + colp;
-            float* fast_dst[2] = {nullptr, nullptr};
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const EpiLink e = make_link(p, link0 + 8 * k);
-                const bool ok = __all_sync(0xffffffffu, e.out >= 0 && e.vec && g * p.g_cols + p.g_cols <= e.n_valid);
-                fast_dst[k] = ok ? p.taps + 2 * (e.out + n0) : nullptr;
-            }
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const uint32_t t_acc = tmem_base + (uint32_t)(acc * p.g_cols);
-            float s_abs = 0.f, s_sq = 0.f, nf = 0.f;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * k) << 16);
-                if (fast_dst[k] != nullptr) {
-                    epi_block_fast(p, taddr, fast_dst[k], p.g_cols);
-                } else {
-                    const EpiLink e = make_link(p, link0 + 8 * k);
-                    epi_block<false>(p, taddr, e, n0, s_abs, s_sq, nf, p.g_cols);
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-    }
-
-    __syncwarp();
-    tc_fence_before();
-    cluster_sync_all();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc_pair(tmem_base, p.tmem_cols);
-    }
-}
-
 // tensor16 finish (experiments.py:201-205): a (frame-set, batch) whose partial or total
 // went non-finite is scored as all-zero taps and counted as n_r * n_tx saturations
 // (stats[:, 3]); then the per-frame error sums against the truth (stats[:, 0..2]).
@@ -2009,8 +1741,6 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
         if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedLdg>();
         if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedTma>();
         if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModePackedLdg>();
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(k_correlate_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     });
     if (attr_err != cudaSuccess)
         return fail(PNCE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
@@ -2427,70 +2157,6 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     prm.raw_row_floats = 2 * kRawChunk + ((prm.c & 1) ? 4 : 0);
-    // Plain launches whose lags need the whole TMEM in one group (256 < R <= 512, e.g. cfg3):
-    // the 4-CTA quad kernel -- two pairs on one row tile, one 256-column lag group each, with
-    // double-buffered accumulators (PNCE_TUNE_QUAD=0: the pair kernel with the split drain)
-    static const int quad_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_QUAD");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (!t16 && !scored && use_tma && quad_env == 1 && p->fused.n_groups == 1 && p->fused.g_cols > 256 &&
-        p->packed_ldg.n_groups == 2 && p->num_sms >= 4) {
-        CorrParams qp;
-        s = fill_params(p, p->packed_ldg, true, taps, nullptr, nullptr, n_frames, qp);
-        if (s != PNCE_OK) return s;
-        qp.iq = iq;
-        qp.samples = prm.samples;
-        qp.c = prm.c;
-        qp.raw_row_floats = prm.raw_row_floats;
-        qp.raw_stage_bytes = (uint32_t)(kLinksPerTile / 2 * qp.raw_row_floats * 4);
-        const int64_t budget = (int64_t)kSmemLimit - 2048;
-        static const int qab = [] {
-            const char* e = std::getenv("PNCE_TUNE_QUAD_AB");
-            return e ? std::atoi(e) : 4;
-        }();
-        const int ab = (int)std::min<int64_t>(std::min(qab, 8), budget / (int64_t)qp.stage_bytes);
-        const int raw = (int)std::min<int64_t>(16, (budget - (int64_t)ab * qp.stage_bytes) / qp.raw_stage_bytes);
-        if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the quad pipeline");
-        qp.stages = ab;
-        qp.raw_stages = raw;
-        CUtensorMap tm_q;
-        s = make_tmap_raw(&tm_q, iq, (uint64_t)samples * 2, (uint64_t)qp.total_links, (uint32_t)qp.raw_row_floats,
-                          kLinksPerTile / 2);
-        if (s != PNCE_OK) return s;
-        const size_t smem = 1024 + (size_t)ab * qp.stage_bytes + 1024 + (size_t)raw * qp.raw_stage_bytes;
-        // persistent grid: only as many 4-CTA clusters as can be co-resident (GPC sizes need not
-        // be multiples of 4, so this can be fewer than num_sms / 4)
-        static int max_quads = -1;
-        static std::mutex mq_mu;
-        {
-            std::lock_guard<std::mutex> lk(mq_mu);
-            if (max_quads < 0) {
-                cudaLaunchConfig_t lc = {};
-                lc.gridDim = dim3(4 * (p->num_sms / 4), 1, 1);
-                lc.blockDim = dim3(kThreadsK3, 1, 1);
-                lc.dynamicSmemBytes = kSmemLimit;
-                int n = 0;
-                if (cudaOccupancyMaxActiveClusters(&n, k_correlate_quad, &lc) != cudaSuccess || n <= 0) {
-                    cudaGetLastError();
-                    n = p->num_sms / 4;
-                }
-                max_quads = n;
-                if (std::getenv("PNCE_VERBOSE")) {
-                    int n2 = 0;
-                    lc.gridDim = dim3(2 * (p->num_sms / 2), 1, 1);
-                    cudaOccupancyMaxActiveClusters(&n2, k_correlate<kModeFusedTma, false>, &lc);
-                    std::fprintf(stderr, "pnce: co-resident clusters: %d quads (4 CTAs), %d pairs\n", n, n2);
-                }
-            }
-        }
-        const int quads = (int)std::max<int64_t>(1, std::min<int64_t>(qp.m_tiles, max_quads));
-        k_correlate_quad<<<4 * quads, kThreadsK3, smem, st>>>(tm_q, p->packed_ldg.tm_circ, qp);
-        diag_dump(st);
-        g_launches++;
-        CUDA_TRY(cudaGetLastError());
-        return PNCE_OK;
-    }
     CUtensorMap tm_raw;
     if (map_ok) {
         s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);

@@ -437,13 +437,6 @@ __device__ __forceinline__ void bulk_copy_s2s(uint32_t dst_cluster, const void* 
         : "memory");
 }
 
-// Commit prior pair MMAs to the barrier at the same offset in every CTA of `mask` (cluster ranks).
-__device__ __forceinline__ void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
-}
-
 // Commit prior MMAs of this thread to the barrier at the same offset in the CTAs of `mask`.
 __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(
