@@ -844,6 +844,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             int kb = 0, ti = 0, stage = 0, mt = 0, g = 0;
             { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
             uint32_t phase = 0;
+#ifdef PNCE_DIAG_PROF
+            uint64_t prof_scr_wait = 0;
+#endif
             PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1u);
@@ -856,7 +859,13 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 const int r = ti / p.n_groups;
                 if (from_scr) {
                     // group 0 of this row tile stored the converted A stage of K-block kb
+#ifdef PNCE_DIAG_PROF
+                    const uint64_t w0 = clock64();
+#endif
                     mbar_wait(&scr_full[(r & 1) * p.k_blocks + kb], (uint32_t)(r >> 1) & 1u);
+#ifdef PNCE_DIAG_PROF
+                    prof_scr_wait += clock64() - w0;
+#endif
                     fence_proxy_async_global();
                 }
                 if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes + (from_scr ? 2 * a_bytes : 0u));
@@ -877,6 +886,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 PROF_MARK(1);
             }
             PROF_END(0, 2);
+#ifdef PNCE_DIAG_PROF
+            g_prof[blockIdx.x * kProfSlots + 15] = prof_scr_wait;
+#endif
         }
     } else if (warp == 1) {
         if (leader && lane == 0 && split) {
@@ -1047,6 +1059,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             int kb = 0, stage = 0, rs = 0, ti = 0, mt = 0, g = 0;
             { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
             uint32_t phase = 0, rphase = 0;
+#ifdef PNCE_DIAG_PROF
+            uint64_t prof_read_wait = 0, prof_bar_wait = 0, prof_done_wait = 0;
+#endif
             PROF_BEGIN(3);
             for (int j = 0; j < jobs; ++j) {
                 const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
@@ -1118,8 +1133,19 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         // when S = 2); a K-block's barrier fires once its store has completed,
                         // kScrLag stores later (all of them at the row tile's last K-block).
                         constexpr int kScrLag = 4;
+#ifdef PNCE_DIAG_PROF
+                        const uint64_t w0 = clock64();
+#endif
                         if (cw == 0 && lane == 0) bulk_wait_read<0>();
+#ifdef PNCE_DIAG_PROF
+                        const uint64_t w1 = clock64();
+#endif
                         named_bar_sync(1, kCW * 32);
+#ifdef PNCE_DIAG_PROF
+                        const uint64_t w2 = clock64();
+                        prof_read_wait += w1 - w0;
+                        prof_bar_wait += w2 - w1;
+#endif
                         if (cw == 0 && lane == 0) {
                             const int r = ti / p.n_groups;
                             if (p.scr_pol)
@@ -1129,6 +1155,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                                 bulk_store_s2g(p.scratch + (size_t)scr_row(r, kb) * 128, sa, a_bytes);
                             bulk_commit();
                             uint64_t* sf = &scr_full[(r & 1) * p.k_blocks];
+#ifdef PNCE_DIAG_PROF
+                            const uint64_t w3 = clock64();
+#endif
                             if (kb == p.k_blocks - 1) {
                                 bulk_wait<0>();
                                 for (int q = max(0, kb - kScrLag); q <= kb; ++q) mbar_arrive(&sf[q]);
@@ -1136,6 +1165,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                                 bulk_wait<kScrLag>();
                                 mbar_arrive(&sf[kb - kScrLag]);
                             }
+#ifdef PNCE_DIAG_PROF
+                            prof_done_wait += clock64() - w3;
+#endif
                         }
                     }
                 }
@@ -1148,6 +1180,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             }
             if (reuse && cw == 0 && lane == 0) bulk_wait<0>();  // shared memory must outlive the stores
             if (cw == 0 && lane == 0) PROF_END(7, 3);
+#ifdef PNCE_DIAG_PROF
+            if (cw == 0 && lane == 0) {
+                g_prof[blockIdx.x * kProfSlots + 13] = prof_read_wait + prof_bar_wait;
+                g_prof[blockIdx.x * kProfSlots + 14] = prof_done_wait;
+            }
+#endif
         } else if (FLDG) {
             // ===== pipelined LDG converters.  Group gsel (warps 4-7 / 8-11) converts the jobs
             // j = gsel (mod 2); each thread holds one K-block of its 16 links' samples in
@@ -1319,7 +1357,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             // (links are re-derived where needed instead of kept live: register pressure)
             const int n0 = g * p.g_cols + colp;
 #ifndef PNCE_DIAG_NO_TRUTH_PF
-            if (SCORED && p.truth != nullptr && (lane & 3) == 0) {
+            // (not with the LDGSTS truth ring: its loads are in flight early enough, and the bulk
+            // prefetches compete with the TMA loads for the copy engine: -5 % scored)
+            if (SCORED && p.truth != nullptr && p.truth_slots == 0 && (lane & 3) == 0) {
 #else
             if (false) {
 #endif
