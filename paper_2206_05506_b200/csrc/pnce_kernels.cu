@@ -261,6 +261,7 @@ struct CorrParams {
                           // stages to `scratch`; the other groups of the row tile TMA them back
     uint32_t bar_bytes;   // barrier block bytes (1 KB; 2 KB with a_reuse: + scratch barriers)
     int32_t scr_pol;      // a_reuse: 1 = evict_last L2 policy on the scratch stores / reloads
+    int32_t scr_slots;    // a_reuse: scratch slots (row tiles) per cluster: 1 when k_blocks >= stages
     uint8_t* scratch;     // a_reuse: [2 slots][clusters][2 CTAs][k_blocks][128 rows][128 B]
     int32_t split_drain;  // release the first N half of a single accumulator early (see k_correlate)
     int32_t truth_slots;  // scored drain: per-thread LDGSTS ring depth for the truth (0: register path)
@@ -825,7 +826,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     };
     // scratch row of (row-tile iteration r, this CTA, K-block kb); slots alternate per row tile
     auto scr_row = [&](int r, int kb) -> int {
-        return ((((r & 1) * n_clusters + cid) * 2 + (int)rank) * p.k_blocks + kb) * kBM;
+        return ((((r % p.scr_slots) * n_clusters + cid) * 2 + (int)rank) * p.k_blocks + kb) * kBM;
     };
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
     const uint32_t a_bytes = kBM * kBK * 2;
@@ -862,7 +863,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #ifdef PNCE_DIAG_PROF
                     const uint64_t w0 = clock64();
 #endif
-                    mbar_wait(&scr_full[(r & 1) * p.k_blocks + kb], (uint32_t)(r >> 1) & 1u);
+                    mbar_wait(&scr_full[(r % p.scr_slots) * p.k_blocks + kb], (uint32_t)(r / p.scr_slots) & 1u);
 #ifdef PNCE_DIAG_PROF
                     prof_scr_wait += clock64() - w0;
 #endif
@@ -1154,7 +1155,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             else
                                 bulk_store_s2g(p.scratch + (size_t)scr_row(r, kb) * 128, sa, a_bytes);
                             bulk_commit();
-                            uint64_t* sf = &scr_full[(r & 1) * p.k_blocks];
+                            uint64_t* sf = &scr_full[(r % p.scr_slots) * p.k_blocks];
 #ifdef PNCE_DIAG_PROF
                             const uint64_t w3 = clock64();
 #endif
@@ -2218,6 +2219,8 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.a_reuse = 1;
             const char* sp = std::getenv("PNCE_TUNE_SCR_POL");
             prm.scr_pol = sp ? std::atoi(sp) : 1;
+            const char* ss = std::getenv("PNCE_TUNE_SCR_SLOTS");
+            prm.scr_slots = ss ? std::max(1, std::min(2, std::atoi(ss))) : 1;
             prm.bar_bytes = 2048;
             budget -= 1024;
         }
@@ -2241,6 +2244,9 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
         prm.raw_stages = raw;
+        // one scratch slot is enough when a K-block's store for row tile r+1 (group 0) comes at
+        // least `stages` jobs after the last group's load of it for row tile r: k_blocks >= stages
+        if (prm.a_reuse && prm.k_blocks < prm.stages) prm.scr_slots = 2;
         prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + prm.bar_bytes +
                                    (size_t)prm.raw_stages * prm.raw_stage_bytes);
         const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)8 * prm.truth_slots * 2048;
@@ -2259,7 +2265,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
                     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
                 }
             });
-            const uint64_t rows = (uint64_t)2 * (grid / 2) * 2 * prm.k_blocks * kBM;
+            const uint64_t rows = (uint64_t)prm.scr_slots * (grid / 2) * 2 * prm.k_blocks * kBM;
             cudaError_t e = cudaMallocAsync(&scratch, rows * 128, st);
             if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("A scratch: ") + cudaGetErrorString(e));
             prm.scratch = static_cast<uint8_t*>(scratch);
