@@ -515,13 +515,10 @@ __device__ __forceinline__ void epi_reps_scored(const CorrParams& p, const uint3
         const float im0 = __uint_as_float(v[4 * i + 2]) * p.inv_m;
         const float im1 = __uint_as_float(v[4 * i + 3]) * p.inv_m;
         if (e.out < 0 || lag >= e.n_valid) continue;
-        nf = fmaf(re0, 0.f, nf);
-        nf = fmaf(im0, 0.f, nf);
+        // (non-finite taps show up in s_sq: the caller flags a recount from it, see below)
         float* dst = p.taps + 2 * (e.out + lag);
         const float q0 = err_acc(re0, im0, h[i].x, h[i].y, s_abs, s_sq);
         if (lag + 1 < e.n_valid) {
-            nf = fmaf(re1, 0.f, nf);
-            nf = fmaf(im1, 0.f, nf);
             if (e.vec) {
                 st_global_v4(dst, re0, im0, re1, im1);
             } else {
@@ -567,6 +564,9 @@ __device__ __forceinline__ void epi_block_scored(const CorrParams& p, uint32_t t
     while (step(h0, h1) && step(h1, h0)) {
     }
     if (p.link_err != nullptr) link_flush(p, e, la, quad);
+    // a non-finite tap (or truth) makes the squared-error sum non-finite; overflow of finite
+    // errors also lands here, which only costs the exact recount
+    if (!isfinite(s_sq)) nf = 1.f;
 }
 
 // Scored drain with the truth staged through shared memory: each thread keeps a private
@@ -612,6 +612,7 @@ __device__ __forceinline__ void epi_block_scored_smem(const CorrParams& p, uint3
     }
     cp_async_wait<0>();
     if (p.link_err != nullptr) link_flush(p, e, la, quad);
+    if (!isfinite(s_sq)) nf = 1.f;  // (as epi_block_scored)
 }
 
 // Fast drain of one 16-lane block when every lag this thread owns is valid, the run is
