@@ -746,8 +746,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
     // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
     // (packed/TMA mode has no converter work: EPI8 moves 4 of those warps to the epilogue)
-    // (scored instantiations flip the flag: EPI8 = true there selects 8 converter + 4 epilogue warps)
-    constexpr int kCW = ((SCORED != EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
+    constexpr int kCW = ((SCORED || EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
     constexpr int kEW0 = kConvWarp0 + kCW;
     constexpr int kEW = kWarps - kEW0;
     // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
@@ -1690,9 +1689,6 @@ static cudaError_t set_smem_attrs() {
     if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
         e = cudaFuncSetAttribute(k_correlate<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemLimit);
-    if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
-        e = cudaFuncSetAttribute(k_correlate<MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemLimit);
     if (e == cudaSuccess && MODE == kModeFusedTma)
         e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -1712,14 +1708,7 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
         return e ? std::atoi(e) : -1;
     }();
     const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
-    // scored: 4 converter + 8 epilogue warps by default; PNCE_TUNE_SCORED_CONV8=1 -> 8 + 4
-    static const bool sc_conv8 = [] {
-        const char* e = std::getenv("PNCE_TUNE_SCORED_CONV8");
-        return e && std::atoi(e) == 1;
-    }();
-    if (scored && sc_conv8 && (MODE == kModeFusedTma || MODE == kModePacked))
-        k_correlate<MODE, true, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
-    else if (scored)
+    if (scored)
         k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else if ((MODE == kModeFusedTma || MODE == kModePacked) && epi8)
         k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
