@@ -1319,8 +1319,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
         uint32_t acc_phase = 0;
         PROF_BEGIN(2);
         if constexpr (T16) {
-            // accumulation units of chunk_kb K-blocks; partial at columns [0, G), running
-            // total at [G, 2G) (single-buffered: the MMA waits for each fold)
+            // accumulation units of chunk_kb K-blocks; partials at columns [acc*G, (acc+1)*G)
+            // (double-buffered when 3G <= 512: the MMA fills one while this folds the other),
+            // running total at [acc_stages*G, (acc_stages+1)*G)
             const int n_units = (p.k_blocks + p.chunk_kb - 1) / p.chunk_kb;
             for (int ti = 0; ti < my_tiles; ++ti) {
                 int mt, g;
@@ -1336,7 +1337,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         const int bb = bb0 + k;
                         const EpiLink e = make_link(p, link0 + 8 * bb);
                         const uint32_t lanes = (uint32_t)(quarter * 32 + 16 * bb) << 16;
-                        t16_fold(p, tmem_base + lanes, tmem_base + lanes + (uint32_t)p.g_cols, e, n0, u == 0,
+                        t16_fold(p, tmem_base + lanes + (uint32_t)(acc * p.g_cols),
+                                 tmem_base + lanes + (uint32_t)(p.acc_stages * p.g_cols), e, n0, u == 0,
                                  u == n_units - 1, sat[k]);
                     }
                     tc_fence_before();
@@ -1728,8 +1730,16 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
     make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
     const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
     make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
-    make_tiling(p->t16, p->r_total, 256, 32);  // 32-column fold chunks
-    p->t16.acc_stages = 1;
+    // tensor16: partial(s) + running total in TMEM.  Default: one partial of <= 256 columns
+    // (the MMA waits for every fold).  PNCE_TUNE_T16_G=160: two partial buffers of <= 160
+    // columns (3 x G <= 512), the MMA filling one while the epilogue folds the other --
+    // measured slower at cfg3 (4.05 vs 3.76 us/frame-set: twice the groups at N=128).
+    static const int t16_g = [] {
+        const char* e = std::getenv("PNCE_TUNE_T16_G");
+        return e ? std::atoi(e) : 256;
+    }();
+    make_tiling(p->t16, p->r_total, t16_g >= 256 ? 256 : 160, 32);  // 32-column fold chunks
+    p->t16.acc_stages = 3 * p->t16.g_cols <= 512 ? 2 : 1;
     p->t16.tmem_cols = 512;
     p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
                               p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols});
