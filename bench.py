@@ -404,6 +404,38 @@ def run_gpu(args, rank, world):
                 "gbs": bytes_gemm_f * Fg / tg / 1e9}
         del packed
 
+    # --- single frame-set latency: one fused launch on ONE resident frame-set
+    # (CUDA events, launch included), and end to end through the public host-buffer API
+    # (pinned host IQ -> HBM -> taps back in pinned host memory, wall clock)
+    lat = None
+    if args.latency_reps > 0:
+        one_iq, one_taps = iq[:1], taps[:1]
+        ts = []
+        for i in range(args.latency_reps + 5):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            _lib.check(L.pnce_process_frames(corr._plan, one_iq.data_ptr(), one_taps.data_ptr(), None, None, None,
+                                             0, 1, stream.cuda_stream))
+            a1.record(stream)
+            a1.synchronize()
+            if i >= 5:
+                ts.append(a0.elapsed_time(a1) * 1e3)
+        h_iq = torch.empty(corr.iq_shape(1), dtype=torch.float32).pin_memory()
+        h_iq.copy_(one_iq.cpu())
+        h_taps = torch.empty(corr.taps_shape(1), dtype=torch.complex64).pin_memory()
+        te = []
+        for i in range(args.latency_reps + 5):
+            torch.cuda.synchronize(dev)
+            w0 = time.perf_counter()
+            corr.process_host(h_iq, h_taps, chunk=1)
+            torch.cuda.synchronize(dev)
+            if i >= 5:
+                te.append((time.perf_counter() - w0) * 1e6)
+        lat = {"frames": 1, "device_us_median": statistics.median(ts), "device_us_min": min(ts),
+               "e2e_us_median": statistics.median(te), "e2e_us_min": min(te), "reps": args.latency_reps,
+               "note": "device: one fused launch on one resident cfg3 frame-set (4 CTA pairs busy); "
+                       "e2e: pinned host IQ -> H2D (CP stripped in the DMA) -> kernel -> D2H taps, wall clock"}
+
     # --- BASELINE configs[3] (cfg4', tensor-bound): fused and packed-GEMM tensor fractions
     c4 = None
     if args.cfg4_frames > 0:
@@ -483,6 +515,7 @@ def run_gpu(args, rank, world):
             "estimate_quality": quality,
             "tensor16_leg": t16,
             "cfg4_leg": c4,
+            "latency": lat,
             "cpu_baseline": cpu, "e2e": e2e, "ingest_iq_file": ingest, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -507,6 +540,7 @@ def main():
     ap.add_argument("--scored-frames", type=int, default=2048, help="frame-sets in the fused-scoring pass")
     ap.add_argument("--gemm-frames", type=int, default=4096)
     ap.add_argument("--cfg4-frames", type=int, default=256, help="frame-sets in the cfg4' leg (0: off)")
+    ap.add_argument("--latency-reps", type=int, default=50, help="single frame-set latency samples (0: off)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
