@@ -431,7 +431,16 @@ def run_gpu(args, rank, world):
             torch.cuda.synchronize(dev)
             if i >= 5:
                 te.append((time.perf_counter() - w0) * 1e6)
+        # the paper's real-time criterion: processing time <= pilot
+        # propagation time P*N_t/(N_batch*F_s); P = C + M + L - 1 samples per received batch
+        p_samples = w["c"] + w["m"] + w["l"] - 1
+        n_batches = -(-w["n_t"] // w["n_batch"])
+        prop_10mhz_us = p_samples * n_batches / 10e6 * 1e6
         lat = {"frames": 1, "device_us_median": statistics.median(ts), "device_us_min": min(ts),
+               "propagation_time_us_at_10MHz": prop_10mhz_us,
+               "realtime_up_to_fs_mhz": {"device": p_samples * n_batches / statistics.median(ts),
+                                         "e2e": p_samples * n_batches / statistics.median(te),
+                                         "amortised": p_samples * n_batches / (ms_per_step * 1e3 / F)},
                "e2e_us_median": statistics.median(te), "e2e_us_min": min(te), "reps": args.latency_reps,
                "note": "device: one fused launch on one resident cfg3 frame-set (4 CTA pairs busy); "
                        "e2e: pinned host IQ -> H2D (CP stripped in the DMA) -> kernel -> D2H taps, wall clock"}
