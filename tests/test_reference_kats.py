@@ -1,7 +1,9 @@
 """The reference's own host-side unit tests, ported onto this package's mirror of its API
 (CPU, no GPU): pkg/tests/test_pn.py (LfsrSpec validation, circular autocorrelation and
 shift), pkg/tests/test_pilots.py (max_batch, PilotConfig, shifts, build_pilot, batch plans,
-propagation time) and pkg/tests/test_metrics.py (mae).  The m-sequences come from the
+propagation time), pkg/tests/test_metrics.py (mae) and the host parts of
+pkg/tests/test_estimator.py (remove_cp, partial circulant / lag-window rows, batch
+separation).  The m-sequences come from the
 oracle's LFSR restatement (the device LFSR is pinned bit-exact to it in
 tests/test_gpu_parity.py), so these run without a GPU."""
 
@@ -272,3 +274,56 @@ class TestMae:  # test_metrics.py:16-34
         truth = torch.tensor([[[1.0 + 0j, 0.0 + 0j]]])
         est = torch.tensor([[[1.0 + 0j, 0.5j]]])
         assert P.mse(truth, est) == pytest.approx(0.125)
+
+
+# ------------------------------------------------------------------ test_estimator.py (host parts)
+class TestRemoveCp:  # test_estimator.py:34-47
+    def test_slicing(self):
+        np.testing.assert_array_equal(P.remove_cp(np.arange(10.0), 3, 7), np.arange(3.0, 10.0))
+
+    def test_identity_channel_recovers_body(self, seq511):
+        frame = P.build_pilot(seq511, 0, 64)
+        np.testing.assert_array_equal(P.remove_cp(frame.samples.numpy(), 64, 511), seq511.numpy())
+
+    def test_too_short(self):
+        with pytest.raises(P.FrameTooShortError):
+            P.remove_cp(np.zeros(9), 3, 7)
+
+
+class TestPartialCirculant:  # test_estimator.py:50-74 (the lag-window rows K1 builds on the device)
+    def test_full_circulant_times_self(self):
+        s7 = seq(3)
+        s = P.build_partial_circulant(s7, 7).double()
+        corr = (s @ s7.chips.double() / 7).numpy()
+        np.testing.assert_allclose(corr, [1] + [-1 / 7] * 6, atol=1e-15)
+
+    def test_single_row_is_sequence(self, seq511):
+        np.testing.assert_array_equal(P.build_partial_circulant(seq511, 1)[0].numpy(), seq511.numpy())
+
+    def test_shape_and_entries(self, seq511):
+        s = P.build_partial_circulant(seq511, 64)
+        assert tuple(s.shape) == (64, 511)
+        assert set(np.unique(s.numpy())) == {-1.0, 1.0}
+
+    def test_rows_are_shifted_base_row(self, seq511):
+        s = P.build_partial_circulant(seq511, 5).numpy()
+        for i in range(5):
+            np.testing.assert_array_equal(s[i], np.roll(s[0], i))
+
+    def test_rows_out_of_range(self, seq511):
+        with pytest.raises(P.RowsOutOfRangeError):
+            P.build_partial_circulant(seq511, 0)
+        with pytest.raises(P.RowsOutOfRangeError):
+            P.build_partial_circulant(seq511, 512)
+
+    def test_batched_rows_are_windows_of_the_full_circulant(self, seq511):
+        # estimator.py:114-117: the stacked lag windows equal rows [s, s+L) of the circulant
+        full = P.build_partial_circulant(seq511, 511).numpy()
+        batch = [P.BatchAssignment(0, 0), P.BatchAssignment(1, 255)]
+        rows = P.batched_lag_rows(seq511, batch, 64).numpy()
+        np.testing.assert_array_equal(rows[:64], full[:64])
+        np.testing.assert_array_equal(rows[64:], full[255:255 + 64])
+
+    def test_separation_violation_rejected(self):
+        with pytest.raises(P.PlanMismatchError):
+            P.validate_batch_separation([P.BatchAssignment(0, 0), P.BatchAssignment(1, 32)], 511, 64)
