@@ -160,6 +160,37 @@ def cpu_reference_rate(w, seconds, threads=None):
     return rate, cores, sample, med
 
 
+def cpu_backend_times(w, seconds=3.0):
+    """SURVEY §8d CPU baseline detail: the oracle port of process_frames with the
+    reference's other backends (reference32; tensor16, the paper-arithmetic emulation with
+    256-sample chunks and binary16 partials) on all host threads, and reference64 on ONE
+    BLAS thread; median ms per cfg3 frame-set over a bounded sample each."""
+    from threadpoolctl import threadpool_limits
+    from oracle import pnce_oracle as O
+    cfg = O.Config(m=w["m"], c=w["c"], n_t=w["n_t"], n_batch=w["n_batch"], l=w["l"], n_r=w["n_r"])
+    chips = O.sequence_for_length(w["m"])
+    rows = O.correlator_rows_for_plan(chips, O.build_batch_plan(cfg), cfg.l)
+    cs, ns = O.derive_seeds(0, cfg.m, cfg.n_batch, cfg.l, 0, 0)
+    _, frames = O.simulate_frame(chips, cfg, cfg.l, w["snr_db"], cs, ns)
+    frames = O.iq_to_frames(O.frames_to_iq(frames))
+
+    def med_ms(**kw):
+        O.process_frames(chips, cfg, frames, rows_per_batch=rows, **kw)   # warm-up
+        ts, t_end = [], time.perf_counter() + seconds
+        while time.perf_counter() < t_end or len(ts) < 2:
+            t0 = time.perf_counter()
+            O.process_frames(chips, cfg, frames, rows_per_batch=rows, **kw)
+            ts.append(time.perf_counter() - t0)
+        return {"ms_per_frame_set": statistics.median(ts) * 1e3, "samples": len(ts)}
+
+    out = {"threads": os.cpu_count(),
+           "reference32": med_ms(backend="reference32"),
+           "tensor16": med_ms(backend="tensor16", chunk_len=256, accumulator="binary16")}
+    with threadpool_limits(limits=1):
+        out["reference64_1_thread"] = med_ms(backend="reference64")
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -184,6 +215,10 @@ def run_reference(args, rank, world):
                          "sample": sample},
         "e2e": {"value": value, "unit": "CSI estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["cpu_backends"] = cpu_backend_times(w)
+    except Exception as exc:  # informational only
+        line["cpu_backends"] = {"skipped": f"{type(exc).__name__}: {exc}"[:200]}
     print(json.dumps(line), flush=True)
     return 0
 
