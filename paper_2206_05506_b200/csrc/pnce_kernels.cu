@@ -12,7 +12,11 @@
 //       one contraction; the frame x batch x rx x re/im axis is the UMMA M dimension);
 //       MODE 2 converts the f32 rows itself (TMA-staged chunks -> fp16/bf16 A stages), so
 //       K2 is fused away; warp-specialised, persistent, mbarrier pipelines, accumulators
-//       in TMEM (512 columns at cfg3, single-buffered).
+//       in TMEM (512 columns at cfg3, single-buffered, with the first N half released to
+//       the next tile's MMAs as soon as it is drained: "split drain").  With several
+//       lag-row groups (R > 512, or the 256-column scored / tensor16 tilings) a cluster
+//       converts a row tile once and re-reads its fp16 A stages from an L2 scratch for the
+//       other groups ("A-stage reuse").
 //   K4  (K3's epilogue) x 1/M, per-transmitter window demux into taps[f, r, t, l]
 //       (experiments.py:206-207), optional sum|e|, sum|e|^2, non-finite count and per-link
 //       MSE vs. truth (metrics.py:19-25 + MSE), or the tensor16 chunk fold (halfprec.py).
