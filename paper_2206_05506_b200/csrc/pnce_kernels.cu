@@ -1652,6 +1652,7 @@ struct pnce_plan {
     Tiling packed;   // packed operand via TMA: same grouping (TMA ingress, not the drain, bounds G=256)
     Tiling packed_ldg;  // <= 256 columns, double-buffered accumulator (packed LDG mode, scored launches)
     Tiling t16;      // tensor16 emulation: <= 256 columns (multiple of 32), partial + running total
+    Tiling narrow;   // plain launches with few tiles: <= 128 columns, groups spread over clusters
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
     void* synth = nullptr;  // synthesiser state (pnce_synth.cu)
@@ -1743,10 +1744,12 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
         return e ? std::atoi(e) : 256;
     }();
     make_tiling(p->t16, p->r_total, t16_g >= 256 ? 256 : 160, 32);  // 32-column fold chunks
+    make_tiling(p->narrow, p->r_total, 128);
     p->t16.acc_stages = 3 * p->t16.g_cols <= 512 ? 2 : 1;
     p->t16.tmem_cols = 512;
     p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
-                              p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols});
+                              p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols,
+                              p->narrow.n_groups * p->narrow.g_cols});
     cudaError_t e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
     if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
     const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
@@ -1776,6 +1779,7 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
     pnce_status_t s = make_tmap(&p->fused.tm_circ, p->circ, p->k_pad, circ_rows, p->fused.nm / 2, bf16);
     if (s == PNCE_OK) s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2, bf16);
     if (s == PNCE_OK) s = make_tmap(&p->t16.tm_circ, p->circ, p->k_pad, circ_rows, p->t16.nm / 2, bf16);
+    if (s == PNCE_OK) s = make_tmap(&p->narrow.tm_circ, p->circ, p->k_pad, circ_rows, p->narrow.nm / 2, bf16);
     if (s == PNCE_OK)
         s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2, bf16);
     if (s != PNCE_OK) return s;
@@ -2182,7 +2186,18 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         const char* e = std::getenv("PNCE_TUNE_SCORED_G");
         return e ? std::atoi(e) : 256;
     }();
-    const Tiling& tiling = t16 ? p->t16 : (scored_launch && scored_g == 256 ? p->packed_ldg : p->fused);
+    // plain launches with few row tiles (a handful of frame-sets: latency-bound): narrower
+    // lag-row groups spread over more CTA pairs (same MMAs per output, bit-identical taps)
+    const int64_t tiles_fused = (n_frames * p->n_batches * (int64_t)p->cfg.n_r + kBM - 1) / kBM * p->fused.n_groups;
+    static const int narrow_env = [] {
+        const char* e = std::getenv("PNCE_TUNE_NARROW");
+        return e ? std::atoi(e) : 1;
+    }();
+    const bool narrow = !t16 && !scored_launch && narrow_env == 1 && p->narrow.n_groups > p->fused.n_groups &&
+                        tiles_fused * 4 <= p->num_sms / 2;
+    const Tiling& tiling = t16 ? p->t16
+                               : (narrow ? p->narrow
+                                         : (scored_launch && scored_g == 256 ? p->packed_ldg : p->fused));
     pnce_status_t s = fill_params(p, tiling, true, taps, t16 ? nullptr : truth, t16 ? nullptr : stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
@@ -2219,7 +2234,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             const char* e = std::getenv("PNCE_TUNE_A_REUSE");
             return e ? std::atoi(e) : 1;
         }();
-        if (reuse_env == 1 && tiling.n_groups > 1 && prm.k_blocks <= 64) {
+        if (reuse_env == 1 && !narrow && tiling.n_groups > 1 && prm.k_blocks <= 64) {
             prm.a_reuse = 1;
             const char* sp = std::getenv("PNCE_TUNE_SCR_POL");
             prm.scr_pol = sp ? std::atoi(sp) : 1;

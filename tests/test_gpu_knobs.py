@@ -1,6 +1,7 @@
 """Pipeline variants that must not change a single bit: the split drain (first accumulator
 half released early), the A-stage reuse across lag-row groups (L2 scratch), and the
-LDGSTS truth ring of the scored drain -- each run in a subprocess with its knob off and
+LDGSTS truth ring of the scored drain, the narrow lag-row groups of few-tile launches --
+each run in a subprocess with its knob off and
 compared with the default build of the same launch (same MMAs in the same K order, same
 epilogue arithmetic).  Covers one group (cfg3), two groups (scored / tensor16 tilings) and
 four groups (cfg4')."""
@@ -23,7 +24,7 @@ import paper_2206_05506_b200 as P
 from paper_2206_05506_b200 import synth as S
 dev = torch.device("cuda:0")
 out = {}
-for name, m, l, nt, nb, nr, deg, F in (("cfg3", 1023, 64, 64, 8, 64, 10, 9),
+for name, m, l, nt, nb, nr, deg, F in (("cfg3", 1023, 64, 64, 8, 64, 10, 9), ("cfg3_1", 1023, 64, 64, 8, 64, 10, 1),
                                        ("cfg4", 2047, 127, 128, 16, 128, 11, 3),
                                        ("odd", 1023, 40, 24, 10, 40, 10, 5)):
     cfg = P.PilotConfig(m=m, c=l, n_t=nt, n_batch=nb, l=l, f_s=10e6)
@@ -59,7 +60,8 @@ def default_run(tmp_path_factory):
     return _run(tmp_path_factory.mktemp("knobs"), "default", {})
 
 
-@pytest.mark.parametrize("knob", ["PNCE_TUNE_SPLIT_DRAIN", "PNCE_TUNE_A_REUSE", "PNCE_TUNE_TRUTH_SLOTS"])
+@pytest.mark.parametrize("knob", ["PNCE_TUNE_SPLIT_DRAIN", "PNCE_TUNE_A_REUSE", "PNCE_TUNE_TRUTH_SLOTS",
+                                  "PNCE_TUNE_NARROW"])
 def test_variant_bit_identical(default_run, tmp_path, knob):
     other = _run(tmp_path, knob, {knob: "0"})
     for key in default_run.files:
