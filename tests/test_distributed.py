@@ -49,7 +49,7 @@ def test_frame_shard_partition(n_frames):
 
 def test_gloo_world2_reduce_and_gather():
     world, n_frames = 2, 7
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), n_frames, out), nprocs=world, join=True)
     want = [sum(range(n_frames)), sum(i * i for i in range(n_frames)), 0.0, 0.0]

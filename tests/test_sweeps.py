@@ -92,7 +92,7 @@ def _worker(rank, world, port, out):
 
 
 def test_gloo_world2_sweep_gather():
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     assert out[1] is None
