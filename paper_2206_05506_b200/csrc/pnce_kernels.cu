@@ -1744,7 +1744,12 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
         return e ? std::atoi(e) : 256;
     }();
     make_tiling(p->t16, p->r_total, t16_g >= 256 ? 256 : 160, 32);  // 32-column fold chunks
-    make_tiling(p->narrow, p->r_total, 128);
+    static const int narrow_g = [] {
+        const char* e = std::getenv("PNCE_TUNE_NARROW_G");
+        const int g = e ? std::atoi(e) : 128;
+        return (g == 64 || g == 96 || g == 192 || g == 256) ? g : 128;
+    }();
+    make_tiling(p->narrow, p->r_total, narrow_g);
     p->t16.acc_stages = 3 * p->t16.g_cols <= 512 ? 2 : 1;
     p->t16.tmem_cols = 512;
     p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
