@@ -2,7 +2,7 @@
 
 Run once per knob setting (knobs are read once per process); writes the taps of 1..4
 frame-sets to gpurun_out/narrow_<tag>.pt so the settings can be compared bit for bit.
-    PNCE_TUNE_NARROW_G=64 python tools/narrow_g_trial.py g64
+    PNCE_TUNE_NARROW_G=64 python tools/narrow_g_trial.py g64 [1,2,4]
 """
 import ctypes
 import statistics
@@ -25,7 +25,7 @@ h = S.draw_channel(corr, 4, seed=11)
 S.simulate_frames(corr, h, 10.0, seed=12, out=iq)
 s = torch.cuda.current_stream(dev)
 out = {}
-for n in (1, 2, 4):
+for n in (tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (1, 2, 4)):
     taps = torch.empty(corr.taps_shape(n), dtype=torch.complex64, device=dev)
     ts = []
     for i in range(55):
