@@ -2218,6 +2218,14 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     const bool map_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
     bool use_tma = map_ok;
     if (fm && std::atoi(fm) == kModeFusedLdg) use_tma = false;
+    // lone-tile (narrow) launches are latency-bound: the LDG converters (no raw staging ring,
+    // all shared memory for A/B stages) shorten the serial K chain, 26 vs 29 us per cfg3
+    // frame-set, bit-identical (tools/narrow_mode_trial.sh; PNCE_TUNE_NARROW_LDG=0: TMA ring)
+    static const int narrow_ldg_env = [] {
+        const char* e = std::getenv("PNCE_TUNE_NARROW_LDG");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (narrow && !fm && narrow_ldg_env == 1) use_tma = false;
     if (t16 && !map_ok)
         return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
