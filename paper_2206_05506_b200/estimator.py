@@ -279,6 +279,18 @@ class Correlator:
             self._host_streams = st
         s_in, s_out, _, bufs_in, bufs_out = st
         L = _lib.lib()
+        if n_frames <= chunk and bodies_only:
+            # one stage (the single frame-set latency case): nothing to overlap, so copy in,
+            # correlate and copy out in order on the current stream -- no side streams/events
+            with torch.cuda.device(self.device):
+                sp = ctypes.c_void_p(cur.cuda_stream)
+                _lib.check(L.pnce_copy_bodies_h2d(self._plan, ctypes.c_void_p(iq_host.data_ptr()),
+                                                  ctypes.c_void_p(bufs_in[0].data_ptr()), stride, n_frames, sp))
+                _lib.check(L.pnce_process_bodies(self._plan, ctypes.c_void_p(bufs_in[0].data_ptr()), stride,
+                                                 ctypes.c_void_p(bufs_out[0].data_ptr()), None, None, None,
+                                                 n_frames, sp))
+                taps_host.copy_(bufs_out[0][:n_frames], non_blocking=True)
+            return taps_host
         in_done = [torch.cuda.Event() for _ in range(2)]
         comp_done = [torch.cuda.Event() for _ in range(2)]
         out_done = [torch.cuda.Event() for _ in range(2)]

@@ -427,10 +427,12 @@ def test_unaligned_buffers(dev):
     assert torch.allclose(st2, st, rtol=1e-6) and torch.allclose(l2, lk, rtol=1e-6)
 
 
+@pytest.mark.parametrize("chunk", [2, 8])
 @pytest.mark.parametrize("bodies_only", [True, False])
-def test_process_host(dev, bodies_only):
+def test_process_host(dev, bodies_only, chunk):
     """Pinned host IQ -> (pitched body-only DMA | full rows) -> kernel -> pinned host taps,
-    chunked and double-buffered: equal to the resident-input path bit for bit."""
+    chunked and double-buffered (chunk 2) or one in-order stage (chunk 8 >= 5 frame-sets):
+    equal to the resident-input path bit for bit."""
     n, m, l, nb = CONFIGS["cfg2"]
     cfg, ocfg = make_cfg(n, m, l, nb)
     _, iq, _ = sim_sets(ocfg, 5)
@@ -438,6 +440,12 @@ def test_process_host(dev, bodies_only):
     want, _ = corr.process(torch.from_numpy(iq).to(dev))
     host = torch.from_numpy(iq).pin_memory()
     out = torch.empty(corr.taps_shape(5), dtype=torch.complex64).pin_memory()
-    corr.process_host(host, out, chunk=2, bodies_only=bodies_only)
+    corr.process_host(host, out, chunk=chunk, bodies_only=bodies_only)
     torch.cuda.synchronize()
     assert torch.equal(out, want.cpu())
+    if chunk == 8:  # the single-stage path after a double-buffered call on the same correlator
+        out2 = torch.zeros_like(out).pin_memory()
+        corr.process_host(host, out2, chunk=2, bodies_only=bodies_only)
+        corr.process_host(host[:1], out2[:1], chunk=8, bodies_only=bodies_only)
+        torch.cuda.synchronize()
+        assert torch.equal(out2, want.cpu())
