@@ -1653,6 +1653,7 @@ struct pnce_plan {
     Tiling packed_ldg;  // <= 256 columns, double-buffered accumulator (packed LDG mode, scored launches)
     Tiling t16;      // tensor16 emulation: <= 256 columns (multiple of 32), partial + running total
     Tiling narrow;   // plain launches with few tiles: <= 128 columns, groups spread over clusters
+    Tiling mid;      // plain launches with a few more tiles: <= 256 columns
     float* chips;    // device [m]
     void* circ;      // device [rows_alloc][k_pad] 16-bit
     void* synth = nullptr;  // synthesiser state (pnce_synth.cu)
@@ -1750,11 +1751,12 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
         return (g == 64 || g == 96 || g == 192 || g == 256) ? g : 128;
     }();
     make_tiling(p->narrow, p->r_total, narrow_g);
+    make_tiling(p->mid, p->r_total, 256);
     p->t16.acc_stages = 3 * p->t16.g_cols <= 512 ? 2 : 1;
     p->t16.tmem_cols = 512;
     p->rows_alloc = std::max({p->fused.n_groups * p->fused.g_cols, p->packed.n_groups * p->packed.g_cols,
                               p->packed_ldg.n_groups * p->packed_ldg.g_cols, p->t16.n_groups * p->t16.g_cols,
-                              p->narrow.n_groups * p->narrow.g_cols});
+                              p->narrow.n_groups * p->narrow.g_cols, p->mid.n_groups * p->mid.g_cols});
     cudaError_t e = cudaMalloc(&p->circ, (size_t)p->rows_alloc * p->k_pad * 2);
     if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("plan alloc: ") + cudaGetErrorString(e));
     const int64_t total = (int64_t)p->rows_alloc * p->k_pad;
@@ -1785,6 +1787,7 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
     if (s == PNCE_OK) s = make_tmap(&p->packed.tm_circ, p->circ, p->k_pad, circ_rows, p->packed.nm / 2, bf16);
     if (s == PNCE_OK) s = make_tmap(&p->t16.tm_circ, p->circ, p->k_pad, circ_rows, p->t16.nm / 2, bf16);
     if (s == PNCE_OK) s = make_tmap(&p->narrow.tm_circ, p->circ, p->k_pad, circ_rows, p->narrow.nm / 2, bf16);
+    if (s == PNCE_OK) s = make_tmap(&p->mid.tm_circ, p->circ, p->k_pad, circ_rows, p->mid.nm / 2, bf16);
     if (s == PNCE_OK)
         s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2, bf16);
     if (s != PNCE_OK) return s;
@@ -2200,8 +2203,17 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     }();
     const bool narrow = !t16 && !scored_launch && narrow_env == 1 && p->narrow.n_groups > p->fused.n_groups &&
                         tiles_fused * 4 <= p->num_sms / 2;
+    // a few more row tiles (5-9 cfg3 frame-sets): 256-column groups, still one wave of CTA
+    // pairs (PNCE_TUNE_MID: 0 off, 1 TMA raw ring, 2 LDG converters)
+    static const int mid_env = [] {
+        const char* e = std::getenv("PNCE_TUNE_MID");
+        return e ? std::atoi(e) : 1;
+    }();
+    const int64_t row_tiles = tiles_fused / p->fused.n_groups;
+    const bool mid = !t16 && !scored_launch && !narrow && mid_env >= 1 && p->mid.n_groups > p->fused.n_groups &&
+                     row_tiles * p->mid.n_groups <= p->num_sms / 2;
     const Tiling& tiling = t16 ? p->t16
-                               : (narrow ? p->narrow
+                               : (narrow ? p->narrow : mid ? p->mid
                                          : (scored_launch && scored_g == 256 ? p->packed_ldg : p->fused));
     pnce_status_t s = fill_params(p, tiling, true, taps, t16 ? nullptr : truth, t16 ? nullptr : stats, n_frames, prm);
     if (s != PNCE_OK) return s;
@@ -2226,6 +2238,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         return e ? std::atoi(e) : 1;
     }();
     if (narrow && !fm && narrow_ldg_env == 1) use_tma = false;
+    if (mid && !fm && mid_env == 2) use_tma = false;
     if (t16 && !map_ok)
         return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -2247,7 +2260,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             const char* e = std::getenv("PNCE_TUNE_A_REUSE");
             return e ? std::atoi(e) : 1;
         }();
-        if (reuse_env == 1 && !narrow && tiling.n_groups > 1 && prm.k_blocks <= 64) {
+        if (reuse_env == 1 && !narrow && !mid && tiling.n_groups > 1 && prm.k_blocks <= 64) {
             prm.a_reuse = 1;
             const char* sp = std::getenv("PNCE_TUNE_SCR_POL");
             prm.scr_pol = sp ? std::atoi(sp) : 1;

@@ -1,7 +1,7 @@
 """Pipeline variants that must not change a single bit: the split drain (first accumulator
 half released early), the A-stage reuse across lag-row groups (L2 scratch), and the
 LDGSTS truth ring of the scored drain, the narrow lag-row groups of few-tile launches and
-their LDG converters --
+their LDG converters, the 256-column tiling of 5-9 frame-set launches --
 each run in a subprocess with its knob off and
 compared with the default build of the same launch (same MMAs in the same K order, same
 epilogue arithmetic).  Covers one group (cfg3), two groups (scored / tensor16 tilings) and
@@ -62,7 +62,7 @@ def default_run(tmp_path_factory):
 
 
 @pytest.mark.parametrize("knob", ["PNCE_TUNE_SPLIT_DRAIN", "PNCE_TUNE_A_REUSE", "PNCE_TUNE_TRUTH_SLOTS",
-                                  "PNCE_TUNE_NARROW", "PNCE_TUNE_NARROW_LDG"])
+                                  "PNCE_TUNE_NARROW", "PNCE_TUNE_NARROW_LDG", "PNCE_TUNE_MID"])
 def test_variant_bit_identical(default_run, tmp_path, knob):
     other = _run(tmp_path, knob, {knob: "0"})
     for key in default_run.files:

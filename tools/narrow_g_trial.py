@@ -20,12 +20,13 @@ dev = torch.device("cuda", 0)
 cfg = P.PilotConfig(m=1023, c=64, n_t=64, n_batch=8, l=64, f_s=10e6)
 corr = P.Correlator(P.default_spec(10), cfg, 64, device=dev)
 L = _lib.lib()
-iq = torch.empty(corr.iq_shape(4), dtype=torch.float32, device=dev)
-h = S.draw_channel(corr, 4, seed=11)
+NS = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (1, 2, 4)
+iq = torch.empty(corr.iq_shape(max(NS)), dtype=torch.float32, device=dev)
+h = S.draw_channel(corr, max(NS), seed=11)
 S.simulate_frames(corr, h, 10.0, seed=12, out=iq)
 s = torch.cuda.current_stream(dev)
 out = {}
-for n in (tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (1, 2, 4)):
+for n in NS:
     taps = torch.empty(corr.taps_shape(n), dtype=torch.complex64, device=dev)
     ts = []
     for i in range(55):
