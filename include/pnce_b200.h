@@ -18,7 +18,16 @@
  *          pnce/estimator.py:27-37, already normalised by 1/M).
  *   truth  same layout as taps (ChannelRealization.taps, pnce/channel.py:79-88).
  *   stats  float64 [n_frames][4] accumulated (+=):
- *          {sum |h_est - h|, sum |h_est - h|^2, non-finite tap count, 0}.
+ *          {sum |h_est - h|, sum |h_est - h|^2, non-finite tap count, saturations}.
+ *          Saturations use the reference's unit (experiments.py:201-205): a (frame-set,
+ *          batch) whose estimate went non-finite (e.g. an input beyond the fp16 range) is
+ *          scored as all-zero taps and counted as n_r * n_tx.  Saturation accounting needs
+ *          `stats`; without it non-finite taps are left as computed.
+ *
+ * Resources: launch scratch (A-stage reuse, saturation flags, tensor maps) is owned by the
+ * plan, one set per calling stream, allocated on the first launch on that stream; no
+ * launch allocates afterwards.  Compute calls must run with the plan's device current
+ * (PNCE_ERR_DIMENSION otherwise).
  */
 #ifndef PNCE_B200_H
 #define PNCE_B200_H
@@ -104,6 +113,14 @@ pnce_status_t pnce_plan_create_rows(const pnce_cfg_t* cfg, const float* rows_dev
 /* Copy the plan's device-generated chips (float32 [m]) into dst_dev. */
 pnce_status_t pnce_plan_chips(const pnce_plan_t* plan, float* dst_dev, void* stream);
 
+/* The plan's correlation operand as built on the device (test/inspection seam for the
+ * integer work of batched_lag_rows, estimator.py:114-117): 16-bit (plan dtype) rows
+ * [n_rows][k_pad], row j*L + l = chips shifted by shift_j + l (A[j*L+l][k] =
+ * chip[(k - s_j - l) mod M]), columns >= m and rows >= N_b*L zero.  With dst == NULL
+ * only the extents are returned. */
+pnce_status_t pnce_plan_operand(const pnce_plan_t* plan, void* dst_dev, int32_t* n_rows, int32_t* k_pad,
+                                void* stream);
+
 /* Bytes of the packed 16-bit operand pnce_pack_iq writes for n_frames.
  * Packed layout: K_pad = roundup(m, 64) columns; links q = (f*n_batches + b)*n_r + r are
  * grouped by 8 and each 16-row block holds the block's 8 Re rows then its 8 Im rows
@@ -164,6 +181,12 @@ pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* plan, const float*
                                            const float* truth, double* stats, int32_t chunk_len,
                                            int32_t binary16_accumulator, int64_t n_frames,
                                            void* stream);
+
+/* tensor16 mode over compact body rows (pnce_process_bodies layout): the operator seam's
+ * correlate_rows with BackendConfig(kind="tensor16") (estimator.py:68-86 -> halfprec.py:127-156). */
+pnce_status_t pnce_process_bodies_tensor16(const pnce_plan_t* plan, const float* bodies, int32_t body_stride,
+                                           float* taps, const float* truth, double* stats, int32_t chunk_len,
+                                           int32_t binary16_accumulator, int64_t n_frames, void* stream);
 
 /* Input synthesis on the device (channel.py:96-214).  Not part of the timed
  * estimation path: it feeds benches and sweeps with statistically equivalent frames

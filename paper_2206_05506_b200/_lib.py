@@ -34,9 +34,10 @@ _STATUS = {
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
     "pnce_version", "pnce_last_error", "pnce_config_check", "pnce_generate_mseq",
-    "pnce_plan_create", "pnce_plan_create_rows", "pnce_plan_destroy", "pnce_plan_chips", "pnce_workspace_bytes",
+    "pnce_plan_create", "pnce_plan_create_rows", "pnce_plan_destroy", "pnce_plan_chips", "pnce_plan_operand",
+    "pnce_workspace_bytes",
     "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored",
-    "pnce_process_frames_tensor16", "pnce_copy_bodies_h2d", "pnce_process_bodies", "pnce_draw_channel", "pnce_simulate_frames", "pnce_kernel_launches",
+    "pnce_process_frames_tensor16", "pnce_process_bodies_tensor16", "pnce_copy_bodies_h2d", "pnce_process_bodies", "pnce_draw_channel", "pnce_simulate_frames", "pnce_kernel_launches",
 )
 
 
@@ -75,12 +76,14 @@ def lib() -> ctypes.CDLL:
         "pnce_plan_create_rows": (i32, [cfgp, vp, i32, i32, ctypes.POINTER(vp), vp]),
         "pnce_plan_destroy": (i32, [vp]),
         "pnce_plan_chips": (i32, [vp, vp, vp]),
+        "pnce_plan_operand": (i32, [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]),
         "pnce_workspace_bytes": (sz, [vp, i64]),
         "pnce_pack_iq": (i32, [vp, vp, vp, i64, vp]),
         "pnce_correlate": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames": (i32, [vp, vp, vp, vp, vp, vp, sz, i64, vp]),
         "pnce_process_frames_scored": (i32, [vp, vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames_tensor16": (i32, [vp, vp, vp, vp, vp, i32, i32, i64, vp]),
+        "pnce_process_bodies_tensor16": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i64, vp]),
         "pnce_copy_bodies_h2d": (i32, [vp, vp, vp, i32, i64, vp]),
         "pnce_process_bodies": (i32, [vp, vp, i32, vp, vp, vp, vp, i64, vp]),
         "pnce_draw_channel": (i32, [vp, i32, u64, vp, i64, vp]),

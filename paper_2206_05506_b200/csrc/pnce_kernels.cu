@@ -53,6 +53,53 @@ constexpr int kSmemLimit = 227 * 1024;
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
+#define s_ok_or_return(expr)              \
+    do {                                  \
+        pnce_status_t s_ = (expr);        \
+        if (s_ != PNCE_OK) return s_;     \
+    } while (0)
+
+// Tuning knobs (diagnostics): read from the environment ONCE per process, so
+// no launch pays a getenv.  -1 = unset where the default depends on the launch.
+struct Knobs {
+    int epi8, group_fused, group_packed, group_packed_ldg, t16_g, narrow_g;
+    int store_hint, raw_pol, split_drain, packed_mode, scored_g, narrow, mid, fused_mode, narrow_ldg;
+    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages;
+};
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+const Knobs& knobs() {
+    static const Knobs k = [] {
+        Knobs r;
+        r.epi8 = env_int("PNCE_TUNE_EPI8", -1);
+        r.group_fused = env_int("PNCE_TUNE_GROUP_FUSED", 512);
+        r.group_packed = env_int("PNCE_TUNE_GROUP_PACKED", 512);
+        r.group_packed_ldg = env_int("PNCE_TUNE_GROUP_PACKED_LDG", 256);
+        r.t16_g = env_int("PNCE_TUNE_T16_G", 256);
+        const int ng = env_int("PNCE_TUNE_NARROW_G", 128);
+        r.narrow_g = (ng == 64 || ng == 96 || ng == 192 || ng == 256) ? ng : 128;
+        r.store_hint = env_int("PNCE_TUNE_STORE_HINT", 1);
+        r.raw_pol = env_int("PNCE_TUNE_RAW_POL", -1);
+        r.split_drain = env_int("PNCE_TUNE_SPLIT_DRAIN", 1);
+        r.packed_mode = env_int("PNCE_TUNE_PACKED_MODE", 0);
+        r.scored_g = env_int("PNCE_TUNE_SCORED_G", 256);
+        r.narrow = env_int("PNCE_TUNE_NARROW", 1);
+        r.mid = env_int("PNCE_TUNE_MID", 1);
+        r.fused_mode = env_int("PNCE_TUNE_FUSED_MODE", -1);
+        r.narrow_ldg = env_int("PNCE_TUNE_NARROW_LDG", 1);
+        r.a_reuse = env_int("PNCE_TUNE_A_REUSE", 1);
+        r.scr_pol = env_int("PNCE_TUNE_SCR_POL", 1);
+        r.scr_slots = env_int("PNCE_TUNE_SCR_SLOTS", -1);
+        r.truth_slots = env_int("PNCE_TUNE_TRUTH_SLOTS", 3);
+        r.ab_stages = env_int("PNCE_TUNE_AB_STAGES", -1);
+        r.raw_stages = env_int("PNCE_TUNE_RAW_STAGES", -1);
+        return r;
+    }();
+    return k;
+}
+
 pnce_status_t fail(pnce_status_t code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -1472,7 +1519,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 for (int k = 0; k < kBlocksPerWarp; ++k) {
                     const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
                     float bad = 0.f;
-                    if (e.out >= 0 && nf[k] != 0.f) bad = recount_nonfinite(p, e, n0);
+                    if (e.out >= 0 && nf[k] != 0.f) {
+                        bad = recount_nonfinite(p, e, n0);
+                        // saturated (frame-set, batch): zeroed, counted and rescored by k_sat_finish
+                        if (bad != 0.f && p.sat_flags != nullptr)
+                            atomicOr(p.sat_flags + (uint32_t)(link0 + 8 * (bb0 + k)) / (uint32_t)p.n_r, 1u);
+                    }
                     float sa = s_abs[k], sq = s_sq[k];
                     // per-frame reduction: warp-uniform frame -> one atomic per warp.  Links
                     // ascend with the lane, so lane 0 holds the block's first (valid) link.
@@ -1560,6 +1612,76 @@ __global__ void k_t16_finish(float* __restrict__ taps, const float* __restrict__
     if (threadIdx.x == 0 && sat) atomicAdd(&stats[f * 4 + 3], (double)n_r * n_tx);
 }
 
+
+// Saturation finish of a scored launch (experiments.py:201-205 for the fp16/bf16 path): one
+// warp per frame-set.  A frame-set none of whose batches was flagged just adds the launch's
+// fused sums to the caller's stats; a flagged (frame-set, batch) -- one of its taps came out
+// non-finite, e.g. an input beyond the fp16 range -- is scored as all-zero taps, counted as
+// n_r * n_tx saturations (stats[:, 3]), and the frame-set's sums and the flagged links'
+// per-link MSE are recomputed from the taps.
+__global__ void k_sat_finish(float* __restrict__ taps, const float* __restrict__ truth, const double* __restrict__ part,
+                             double* __restrict__ stats, float* __restrict__ link_err,
+                             const uint32_t* __restrict__ flags, int64_t n_frames, int n_r, int n_t, int n_batch,
+                             int n_batches, int l) {
+    const int lane = threadIdx.x & 31;
+    const int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (f >= n_frames) return;
+    const uint32_t* fl = flags + f * n_batches;
+    bool any = false;
+    for (int b = lane; b < n_batches; b += 32) any |= fl[b] != 0;
+    any = __any_sync(0xffffffffu, any);
+    if (!any) {
+        if (lane < 4) stats[f * 4 + lane] += part[f * 4 + lane];
+        return;
+    }
+    const int64_t per_f = (int64_t)n_r * n_t * l;
+    float2* tp = reinterpret_cast<float2*>(taps) + f * per_f;
+    const float2* hp = truth ? reinterpret_cast<const float2*>(truth) + f * per_f : nullptr;
+    double s_abs = 0.0, s_sq = 0.0, bad = 0.0;
+    for (int64_t i = lane; i < per_f; i += 32) {
+        const int t = (int)((i / l) % n_t);
+        float2 v = tp[i];
+        if (fl[t / n_batch]) {
+            v = make_float2(0.f, 0.f);
+            tp[i] = v;
+        }
+        if (!(isfinite(v.x) && isfinite(v.y))) bad += 1.0;
+        if (hp) {
+            const double dx = (double)v.x - hp[i].x, dy = (double)v.y - hp[i].y;
+            s_sq += dx * dx + dy * dy;
+            s_abs += sqrt(dx * dx + dy * dy);
+        }
+    }
+    if (link_err && hp) {
+        for (int64_t q = lane; q < (int64_t)n_r * n_t; q += 32) {
+            const int t = (int)(q % n_t);
+            if (!fl[t / n_batch]) continue;
+            float acc = 0.f;
+            for (int k = 0; k < l; ++k) {
+                const float2 h = hp[q * l + k];
+                acc += h.x * h.x + h.y * h.y;
+            }
+            link_err[f * (int64_t)n_r * n_t + q] = acc / (float)l;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+        s_sq += __shfl_xor_sync(0xffffffffu, s_sq, o);
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+        double sat = 0.0;
+        for (int b = 0; b < n_batches; ++b)
+            if (fl[b]) sat += (double)n_r * min(n_batch, n_t - b * n_batch);
+        if (hp) {
+            stats[f * 4 + 0] += s_abs;
+            stats[f * 4 + 1] += s_sq;
+        }
+        stats[f * 4 + 2] += bad;
+        stats[f * 4 + 3] += sat;
+    }
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1641,8 +1763,33 @@ struct Tiling {
     CUtensorMap tm_circ;  // circulant rows, box = nm/2 rows x 64 K
 };
 
+// Per-(plan, stream) launch resources, created on first use and reused by every later launch
+// on that stream (stream order serialises their users; launches on different streams get
+// different entries, so the library stays reentrant): the A-stage scratch of a_reuse, the
+// saturation flags and per-launch stats of the scored / tensor16 finish, and the last-built
+// tensor maps of the caller's input (rebuilt only when the pointer or extent changes).
+struct StreamRes {
+    cudaStream_t stream = nullptr;
+    uint64_t last_use = 0;
+    uint8_t* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    CUtensorMap tm_scr;
+    uint64_t tm_scr_rows = 0;
+    uint32_t* flags = nullptr;  // [F][n_batches] saturation flags
+    size_t flags_n = 0;
+    double* stats = nullptr;    // [F][4] this launch's sums before the saturation finish
+    size_t stats_n = 0;
+    CUtensorMap tm_in;          // raw f32 rows or the packed operand
+    const void* tm_in_ptr = nullptr;
+    uint64_t tm_in_key[3] = {0, 0, 0};
+};
+
 struct pnce_plan {
     pnce_cfg_t cfg;
+    int device = 0;  // the device the plan's operand lives on; launches must run there
+    std::mutex res_mu;
+    std::vector<StreamRes*> res;
+    uint64_t res_clock = 0;
     int n_batches;
     int r_total;     // N_b * L
     int k_pad;       // roundup(M, 64)
@@ -1667,6 +1814,63 @@ PlanView plan_view(const pnce_plan_t* p) {
 pnce_status_t set_error(pnce_status_t code, const std::string& msg) { return fail(code, msg); }
 void count_launch() { g_launches++; }
 }  // namespace pnce_internal
+
+static pnce_status_t device_setup(int dev);
+
+// The plan's resource entry for `st` (created on first use; at most kMaxStreamRes entries, the
+// least recently used one is released -- cudaFree waits for the device, so its last launch
+// has finished).
+constexpr int kMaxStreamRes = 16;
+static StreamRes* stream_res(pnce_plan* p, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(p->res_mu);
+    for (StreamRes* r : p->res)
+        if (r->stream == st) {
+            r->last_use = ++p->res_clock;
+            return r;
+        }
+    if ((int)p->res.size() >= kMaxStreamRes) {
+        auto it = std::min_element(p->res.begin(), p->res.end(),
+                                   [](const StreamRes* a, const StreamRes* b) { return a->last_use < b->last_use; });
+        StreamRes* old = *it;
+        if (old->scratch) cudaFree(old->scratch);
+        if (old->flags) cudaFree(old->flags);
+        if (old->stats) cudaFree(old->stats);
+        delete old;
+        p->res.erase(it);
+    }
+    StreamRes* r = new StreamRes();
+    r->stream = st;
+    r->last_use = ++p->res_clock;
+    p->res.push_back(r);
+    return r;
+}
+
+// Grow-only device buffer of a StreamRes; a reallocation first waits for the stream (the old
+// buffer may still be read by an earlier launch on it).  Rare: the first launch and growth.
+template <typename T>
+static pnce_status_t ensure_buf(T*& buf, size_t& have, size_t need, cudaStream_t st, const char* what) {
+    if (need <= have && buf) return PNCE_OK;
+    if (buf) {
+        cudaStreamSynchronize(st);
+        cudaFree(buf);
+        buf = nullptr;
+        have = 0;
+    }
+    cudaError_t e = cudaMalloc(&buf, need * sizeof(T));
+    if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    have = need;
+    return PNCE_OK;
+}
+
+// Launch preconditions shared by the compute entry points: the plan's device is current.
+static pnce_status_t check_device(const pnce_plan* p) {
+    int dev = -1;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev != p->device)
+        return fail(PNCE_ERR_DIMENSION, "plan lives on device " + std::to_string(p->device) +
+                                            " but the current device is " + std::to_string(dev));
+    return PNCE_OK;
+}
 
 static void make_tiling(Tiling& t, int r_total, int max_group, int align = 16) {
     const int r16 = (r_total + align - 1) / align * align;
@@ -1711,10 +1915,7 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
     const CUtensorMap& c = scr ? *scr : b;  // scratch map (a_reuse) or an unused placeholder
     // 8 epilogue warps: +1 % for the packed operand (its converter warps are idle anyway),
     // -5 % for the fused path (converters become the bottleneck); PNCE_TUNE_EPI8 overrides
-    static const int epi8_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_EPI8");
-        return e ? std::atoi(e) : -1;
-    }();
+    const int epi8_env = knobs().epi8;
     const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
     if (scored)
         k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
@@ -1730,27 +1931,16 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
     const pnce_cfg_t& cfg = p->cfg;
     p->k_pad = (cfg.m + kBK - 1) / kBK * kBK;
     // Tuning knobs (diagnostics): maximum accumulator columns per lag-row group.
-    const char* gf = std::getenv("PNCE_TUNE_GROUP_FUSED");
-    const char* gp = std::getenv("PNCE_TUNE_GROUP_PACKED");
-    make_tiling(p->fused, p->r_total, gf ? std::atoi(gf) : 512);
-    make_tiling(p->packed, p->r_total, gp ? std::atoi(gp) : 512);
-    const char* gl = std::getenv("PNCE_TUNE_GROUP_PACKED_LDG");
-    make_tiling(p->packed_ldg, p->r_total, gl ? std::atoi(gl) : 256);
+    const Knobs& kn = knobs();
+    make_tiling(p->fused, p->r_total, kn.group_fused);
+    make_tiling(p->packed, p->r_total, kn.group_packed);
+    make_tiling(p->packed_ldg, p->r_total, kn.group_packed_ldg);
     // tensor16: partial(s) + running total in TMEM.  Default: one partial of <= 256 columns
     // (the MMA waits for every fold).  PNCE_TUNE_T16_G=160: two partial buffers of <= 160
     // columns (3 x G <= 512), the MMA filling one while the epilogue folds the other --
     // measured slower at cfg3 (4.05 vs 3.76 us/frame-set: twice the groups at N=128).
-    static const int t16_g = [] {
-        const char* e = std::getenv("PNCE_TUNE_T16_G");
-        return e ? std::atoi(e) : 256;
-    }();
-    make_tiling(p->t16, p->r_total, t16_g >= 256 ? 256 : 160, 32);  // 32-column fold chunks
-    static const int narrow_g = [] {
-        const char* e = std::getenv("PNCE_TUNE_NARROW_G");
-        const int g = e ? std::atoi(e) : 128;
-        return (g == 64 || g == 96 || g == 192 || g == 256) ? g : 128;
-    }();
-    make_tiling(p->narrow, p->r_total, narrow_g);
+    make_tiling(p->t16, p->r_total, kn.t16_g >= 256 ? 256 : 160, 32);  // 32-column fold chunks
+    make_tiling(p->narrow, p->r_total, kn.narrow_g);
     make_tiling(p->mid, p->r_total, 256);
     p->t16.acc_stages = 3 * p->t16.g_cols <= 512 ? 2 : 1;
     p->t16.tmem_cols = 512;
@@ -1791,16 +1981,23 @@ static pnce_status_t plan_build(pnce_plan* p, const float* rows, cudaStream_t st
     if (s == PNCE_OK)
         s = make_tmap(&p->packed_ldg.tm_circ, p->circ, p->k_pad, circ_rows, p->packed_ldg.nm / 2, bf16);
     if (s != PNCE_OK) return s;
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_err = set_smem_attrs<kModePacked>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedLdg>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModeFusedTma>();
-        if (attr_err == cudaSuccess) attr_err = set_smem_attrs<kModePackedLdg>();
-    });
-    if (attr_err != cudaSuccess)
-        return fail(PNCE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return device_setup(p->device);
+}
+
+// Once per DEVICE (function attributes are per device): the 227 KB dynamic shared-memory
+// opt-in of every k_correlate instantiation.  Called with `dev` current.
+static pnce_status_t device_setup(int dev) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return PNCE_OK;
+    cudaError_t e = set_smem_attrs<kModePacked>();
+    if (e == cudaSuccess) e = set_smem_attrs<kModeFusedLdg>();
+    if (e == cudaSuccess) e = set_smem_attrs<kModeFusedTma>();
+    if (e == cudaSuccess) e = set_smem_attrs<kModePackedLdg>();
+    if (e != cudaSuccess)
+        return fail(PNCE_ERR_CUDA, "cudaFuncSetAttribute on device " + std::to_string(dev) + ": " + cudaGetErrorString(e));
+    done.push_back(dev);
     return PNCE_OK;
 }
 
@@ -1879,6 +2076,7 @@ pnce_status_t pnce_plan_create(const pnce_cfg_t* cfg, pnce_plan_t** out, void* s
 
     pnce_plan* p = new pnce_plan();
     p->cfg = *cfg;
+    p->device = dev;
     p->n_batches = (cfg->n_t + cfg->n_batch - 1) / cfg->n_batch;
     p->r_total = cfg->n_batch * cfg->l;
     p->num_sms = sms;
@@ -1917,6 +2115,7 @@ pnce_status_t pnce_plan_create_rows(const pnce_cfg_t* cfg, const float* rows, in
     // one "batch" of one "transmitter" whose window is the whole row set: taps[f][r][0][q] = row q
     pnce_plan* p = new pnce_plan();
     p->cfg = *cfg;
+    p->device = dev;
     p->cfg.c = 0;
     p->cfg.l = n_rows;
     p->cfg.n_t = 1;
@@ -1939,6 +2138,12 @@ pnce_status_t pnce_plan_destroy(pnce_plan_t* p) {
     if (p->chips) cudaFree(p->chips);
     if (p->circ) cudaFree(p->circ);
     if (p->synth) pnce_internal::synth_cache_free(p->synth);
+    for (StreamRes* r : p->res) {
+        if (r->scratch) cudaFree(r->scratch);
+        if (r->flags) cudaFree(r->flags);
+        if (r->stats) cudaFree(r->stats);
+        delete r;
+    }
     delete p;
     return PNCE_OK;
 }
@@ -1947,6 +2152,16 @@ pnce_status_t pnce_plan_chips(const pnce_plan_t* p, float* dst, void* stream) {
     if (!p || !dst) return fail(PNCE_ERR_INVALID_CONFIG, "null plan or destination");
     if (!p->chips) return fail(PNCE_ERR_INVALID_CONFIG, "plan was built from caller rows (no PN chips)");
     CUDA_TRY(cudaMemcpyAsync(dst, p->chips, sizeof(float) * p->cfg.m, cudaMemcpyDeviceToDevice,
+                             static_cast<cudaStream_t>(stream)));
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_plan_operand(const pnce_plan_t* p, void* dst, int32_t* n_rows, int32_t* k_pad, void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_rows) *n_rows = p->rows_alloc;
+    if (k_pad) *k_pad = p->k_pad;
+    if (!dst) return PNCE_OK;
+    CUDA_TRY(cudaMemcpyAsync(dst, p->circ, (size_t)p->rows_alloc * p->k_pad * 2, cudaMemcpyDeviceToDevice,
                              static_cast<cudaStream_t>(stream)));
     return PNCE_OK;
 }
@@ -1966,6 +2181,7 @@ pnce_status_t pnce_pack_iq(const pnce_plan_t* p, const float* iq, void* packed, 
     if (!iq || !packed) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(packed) & 15) return fail(PNCE_ERR_DIMENSION, "packed buffer must be 16-byte aligned");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
+    s_ok_or_return(check_device(p));
     const pnce_cfg_t& c = p->cfg;
     const int samples = c.c + c.m + c.l - 1;
     const int64_t links = n_frames * p->n_batches * (int64_t)c.n_r;
@@ -2022,17 +2238,12 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     if (m_tiles * t.n_groups > INT32_MAX || 2 * prm.total_links > INT32_MAX)
         return fail(PNCE_ERR_DIMENSION, "too many frames for one call");
     prm.m_tiles = (int32_t)m_tiles;
-    const char* sh = std::getenv("PNCE_TUNE_STORE_HINT");
-    prm.store_hint = sh ? std::atoi(sh) : 1;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
+    const Knobs& kn = knobs();
+    prm.store_hint = kn.store_hint;  // evict_first taps: +1.5 % (keeps L2 for the circulant)
     prm.n_groups = t.n_groups;
     prm.bar_bytes = 1024;
-    const char* rp = std::getenv("PNCE_TUNE_RAW_POL");
-    prm.raw_pol = rp ? std::atoi(rp) : (t.n_groups > 1 ? 1 : 0);
-    static const int split_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_SPLIT_DRAIN");
-        return e ? std::atoi(e) : 1;
-    }();
-    prm.split_drain = split_env;
+    prm.raw_pol = kn.raw_pol >= 0 ? kn.raw_pol : (t.n_groups > 1 ? 1 : 0);
+    prm.split_drain = kn.split_drain;
     prm.g_cols = t.g_cols;
     prm.n_mma = t.n_mma;
     prm.nm = t.nm;
@@ -2069,6 +2280,33 @@ static int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
     return (int)(2 * std::max<int64_t>(pairs, 1));
 }
 
+
+// Scored launches with stats: the kernel accumulates into a per-launch stats buffer and
+// raises per-(frame-set, batch) saturation flags; scored_finish then folds them into the
+// caller's stats (k_sat_finish).
+static pnce_status_t scored_prepare(const pnce_plan_t* p, StreamRes* res, int64_t n_frames, cudaStream_t st,
+                                    CorrParams& prm) {
+    const size_t n_fb = (size_t)n_frames * p->n_batches;
+    s_ok_or_return(ensure_buf(res->flags, res->flags_n, n_fb, st, "saturation flags"));
+    s_ok_or_return(ensure_buf(res->stats, res->stats_n, (size_t)n_frames * 4, st, "launch stats"));
+    CUDA_TRY(cudaMemsetAsync(res->flags, 0, n_fb * sizeof(uint32_t), st));
+    CUDA_TRY(cudaMemsetAsync(res->stats, 0, (size_t)n_frames * 4 * sizeof(double), st));
+    prm.sat_flags = res->flags;
+    prm.stats = res->stats;
+    return PNCE_OK;
+}
+
+static pnce_status_t scored_finish(const pnce_plan_t* p, StreamRes* res, float* taps, const float* truth,
+                                   double* stats, float* link_err, int64_t n_frames, cudaStream_t st) {
+    const pnce_cfg_t& c = p->cfg;
+    const unsigned blocks = (unsigned)((n_frames + 7) / 8);
+    k_sat_finish<<<blocks, 256, 0, st>>>(taps, truth, res->stats, stats, link_err, res->flags, n_frames, c.n_r,
+                                         c.n_t, c.n_batch, p->n_batches, c.l);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return PNCE_OK;
+}
+
 pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* taps, const float* truth,
                              double* stats, int64_t n_frames, void* stream) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
@@ -2080,8 +2318,8 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     // LDG-fed A + double-buffered 256-column accumulators (PNCE_TUNE_PACKED_MODE=3; parity-
     // green but 1.3x slower: one N=256 MMA per K-step cannot share A reads and the extra
     // A stores push shared-memory bandwidth past the tensor rate)
-    const char* pm = std::getenv("PNCE_TUNE_PACKED_MODE");
-    const bool ldg = pm && std::atoi(pm) == kModePackedLdg;
+    s_ok_or_return(check_device(p));
+    const bool ldg = knobs().packed_mode == kModePackedLdg;
     const Tiling& t = ldg ? p->packed_ldg : p->packed;
     CorrParams prm;
     pnce_status_t s = fill_params(p, t, false, taps, truth, stats, n_frames, prm);
@@ -2089,22 +2327,39 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
     // packed rows: 2 per link, padded to whole 8-link blocks (a_row order)
     const uint64_t packed_rows = (uint64_t)((prm.total_links + 7) / 8) * 16;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamRes* res = stream_res(const_cast<pnce_plan*>(p), st);
+    const bool scored = truth || stats;
+    if (stats) {
+        s = scored_prepare(p, res, n_frames, st, prm);
+        if (s != PNCE_OK) return s;
+    }
     if (ldg) {
         prm.packed = static_cast<const uint16_t*>(packed);
         prm.packed_rows = (int64_t)packed_rows;
         prm.tx_bytes = 2 * (uint32_t)(t.g_cols / 2) * kBK * 2;  // circulant only
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        launch_k3<kModePackedLdg>(truth || stats, pair_grid(p, prm), smem, st, t.tm_circ, t.tm_circ, prm);
+        launch_k3<kModePackedLdg>(scored, pair_grid(p, prm), smem, st, t.tm_circ, t.tm_circ, prm);
     } else {
-        CUtensorMap tm_in;
-        s = make_tmap(&tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
-        if (s != PNCE_OK) return s;
+        const uint64_t key[3] = {packed_rows, (uint64_t)p->k_pad, 1};
+        if (res->tm_in_ptr != packed || std::memcmp(res->tm_in_key, key, sizeof(key)) != 0) {
+            s = make_tmap(&res->tm_in, packed, p->k_pad, packed_rows, kBM, p->cfg.dtype == PNCE_DTYPE_BF16);
+            if (s != PNCE_OK) {
+                res->tm_in_ptr = nullptr;
+                return s;
+            }
+            res->tm_in_ptr = packed;
+            std::memcpy(res->tm_in_key, key, sizeof(key));
+        }
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
-        launch_k3<kModePacked>(truth || stats, pair_grid(p, prm), smem, st, tm_in, t.tm_circ, prm);
+        launch_k3<kModePacked>(scored, pair_grid(p, prm), smem, st, res->tm_in, t.tm_circ, prm);
     }
-    diag_dump(st);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
+    if (stats) {
+        s = scored_finish(p, res, taps, truth, stats, nullptr, n_frames, st);
+        if (s != PNCE_OK) return s;
+    }
+    diag_dump(st);
     return PNCE_OK;
 }
 
@@ -2161,9 +2416,8 @@ pnce_status_t pnce_copy_bodies_h2d(const pnce_plan_t* p, const float* iq_host, f
     return PNCE_OK;
 }
 
-pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
-                                           double* stats, int32_t chunk_len, int32_t binary16_accumulator,
-                                           int64_t n_frames, void* stream) {
+// tensor16 options of a plan (halfprec.py:44-55, 135-146 checks; device chunks are whole K-blocks)
+static pnce_status_t t16_opts(const pnce_plan_t* p, int32_t chunk_len, int32_t binary16_accumulator, T16Opts& o) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     const int kp4 = (p->cfg.m + 3) / 4 * 4;  // the reference pads K to its 4-wide tile (halfprec.py:80-81)
     if (chunk_len < 0) return fail(PNCE_ERR_INVALID_CONFIG, "chunk_len must be >= 0 (0: one chunk)");
@@ -2171,8 +2425,26 @@ pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq
     if (chunk_len % kBK) return fail(PNCE_ERR_INVALID_CONFIG, "device chunks are whole 64-sample K-blocks");
     if (binary16_accumulator != 0 && binary16_accumulator != 1)
         return fail(PNCE_ERR_INVALID_CONFIG, "accumulator must be 0 (binary32) or 1 (binary16)");
-    T16Opts o{chunk_len ? chunk_len / kBK : p->k_pad / kBK, binary16_accumulator};
+    o = T16Opts{chunk_len ? chunk_len / kBK : p->k_pad / kBK, binary16_accumulator};
+    return PNCE_OK;
+}
+
+pnce_status_t pnce_process_frames_tensor16(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
+                                           double* stats, int32_t chunk_len, int32_t binary16_accumulator,
+                                           int64_t n_frames, void* stream) {
+    T16Opts o;
+    s_ok_or_return(t16_opts(p, chunk_len, binary16_accumulator, o));
     return process_frames_impl(p, iq, taps, truth, stats, nullptr, n_frames, stream, &o);
+}
+
+pnce_status_t pnce_process_bodies_tensor16(const pnce_plan_t* p, const float* bodies, int32_t body_stride,
+                                           float* taps, const float* truth, double* stats, int32_t chunk_len,
+                                           int32_t binary16_accumulator, int64_t n_frames, void* stream) {
+    T16Opts o;
+    s_ok_or_return(t16_opts(p, chunk_len, binary16_accumulator, o));
+    if (body_stride < p->cfg.m) return fail(PNCE_ERR_DIMENSION, "body_stride must be >= m");
+    BodyLayout b{body_stride};
+    return process_frames_impl(p, bodies, taps, truth, stats, nullptr, n_frames, stream, &o, &b);
 }
 
 }  // extern "C"
@@ -2185,36 +2457,26 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (n_frames == 0) return PNCE_OK;
     if (!iq || !taps) return fail(PNCE_ERR_DIMENSION, "null buffer");
     if (reinterpret_cast<uintptr_t>(iq) & 7) return fail(PNCE_ERR_DIMENSION, "iq buffer must be 8-byte aligned");
+    s_ok_or_return(check_device(p));
+    const Knobs& kn = knobs();
     CorrParams prm;
     // tensor16: scoring moves to the finish kernel (saturated batches are scored as zeros).
     // Scored launches (drain ~2x the main loop) use <= 256-column groups with two TMEM
     // accumulators, so one tile's drain overlaps the next tile's MMAs (knob PNCE_TUNE_SCORED_G)
-    const bool scored_launch = !t16 && (truth || stats || link_err);
-    static const int scored_g = [] {
-        const char* e = std::getenv("PNCE_TUNE_SCORED_G");
-        return e ? std::atoi(e) : 256;
-    }();
+    const bool scored = !t16 && (truth || stats || link_err);
     // plain launches with few row tiles (a handful of frame-sets: latency-bound): narrower
     // lag-row groups spread over more CTA pairs (same MMAs per output, bit-identical taps)
     const int64_t tiles_fused = (n_frames * p->n_batches * (int64_t)p->cfg.n_r + kBM - 1) / kBM * p->fused.n_groups;
-    static const int narrow_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_NARROW");
-        return e ? std::atoi(e) : 1;
-    }();
-    const bool narrow = !t16 && !scored_launch && narrow_env == 1 && p->narrow.n_groups > p->fused.n_groups &&
+    const bool narrow = !t16 && !scored && kn.narrow == 1 && p->narrow.n_groups > p->fused.n_groups &&
                         tiles_fused * 4 <= p->num_sms / 2;
     // a few more row tiles (5-9 cfg3 frame-sets): 256-column groups, still one wave of CTA
     // pairs (PNCE_TUNE_MID: 0 off, 1 TMA raw ring, 2 LDG converters)
-    static const int mid_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_MID");
-        return e ? std::atoi(e) : 1;
-    }();
     const int64_t row_tiles = tiles_fused / p->fused.n_groups;
-    const bool mid = !t16 && !scored_launch && !narrow && mid_env >= 1 && p->mid.n_groups > p->fused.n_groups &&
+    const bool mid = !t16 && !scored && !narrow && kn.mid >= 1 && p->mid.n_groups > p->fused.n_groups &&
                      row_tiles * p->mid.n_groups <= p->num_sms / 2;
     const Tiling& tiling = t16 ? p->t16
                                : (narrow ? p->narrow : mid ? p->mid
-                                         : (scored_launch && scored_g == 256 ? p->packed_ldg : p->fused));
+                                         : (scored && kn.scored_g == 256 ? p->packed_ldg : p->fused));
     pnce_status_t s = fill_params(p, tiling, true, taps, t16 ? nullptr : truth, t16 ? nullptr : stats, n_frames, prm);
     if (s != PNCE_OK) return s;
     prm.iq = iq;
@@ -2223,32 +2485,35 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         prm.samples = bodies->stride;
         prm.c = 0;
     }
-    const bool scored = !t16 && (truth || stats || link_err);
     const int samples = prm.samples;
-    const char* fm = std::getenv("PNCE_TUNE_FUSED_MODE");
     // the raw f32 rows can be described by a tensor map when the row stride is 16-byte aligned
     const bool map_ok = ((size_t)samples * 8) % 16 == 0 && (reinterpret_cast<uintptr_t>(iq) & 15) == 0;
+    if (t16 && !map_ok)
+        return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
     bool use_tma = map_ok;
-    if (fm && std::atoi(fm) == kModeFusedLdg) use_tma = false;
+    // (the tensor16 instantiation only exists with the TMA raw ring: the knob never applies to it)
+    if (!t16 && kn.fused_mode == kModeFusedLdg) use_tma = false;
     // lone-tile (narrow) launches are latency-bound: the LDG converters (no raw staging ring,
     // all shared memory for A/B stages) shorten the serial K chain, 26 vs 29 us per cfg3
     // frame-set, bit-identical (tools/narrow_mode_trial.sh; PNCE_TUNE_NARROW_LDG=0: TMA ring)
-    static const int narrow_ldg_env = [] {
-        const char* e = std::getenv("PNCE_TUNE_NARROW_LDG");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (narrow && !fm && narrow_ldg_env == 1) use_tma = false;
-    if (mid && !fm && mid_env == 2) use_tma = false;
-    if (t16 && !map_ok)
-        return fail(PNCE_ERR_INVALID_CONFIG, "tensor16 mode needs 16-byte aligned IQ rows (even P+L-1)");
+    if (narrow && kn.fused_mode < 0 && kn.narrow_ldg == 1) use_tma = false;
+    if (mid && kn.fused_mode < 0 && kn.mid == 2) use_tma = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamRes* res = stream_res(const_cast<pnce_plan*>(p), st);
+    if (scored && stats) s_ok_or_return(scored_prepare(p, res, n_frames, st, prm));
     prm.raw_row_floats = 2 * kRawChunk + ((prm.c & 1) ? 4 : 0);
-    CUtensorMap tm_raw;
-    if (map_ok) {
-        s = make_tmap_raw(&tm_raw, iq, (uint64_t)samples * 2, (uint64_t)prm.total_links, (uint32_t)prm.raw_row_floats);
-        if (s != PNCE_OK) return s;
-    }
     if (use_tma) {
+        // raw f32 rows as a tensor map, cached per stream (rebuilt when the input changes)
+        const uint64_t key[3] = {(uint64_t)samples * 2, (uint64_t)prm.total_links, (uint64_t)prm.raw_row_floats << 1};
+        if (res->tm_in_ptr != iq || std::memcmp(res->tm_in_key, key, sizeof(key)) != 0) {
+            s = make_tmap_raw(&res->tm_in, iq, key[0], key[1], (uint32_t)prm.raw_row_floats);
+            if (s != PNCE_OK) {
+                res->tm_in_ptr = nullptr;
+                return s;
+            }
+            res->tm_in_ptr = iq;
+            std::memcpy(res->tm_in_key, key, sizeof(key));
+        }
         // f32 rows TMA-staged in shared memory (default): A/B ring of up to 3 stages, the
         // rest of shared memory as the raw half-K-block ring (its depth hides HBM latency:
         // ~1.3 us per load vs ~0.4 us of MMA per chunk)
@@ -2256,36 +2521,24 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         int64_t budget = (int64_t)kSmemLimit - 2048;
         // a_reuse (several lag-row groups): convert a row tile once, keep its fp16 A stages in an
         // L2-resident scratch for the other groups (PNCE_TUNE_A_REUSE=0: convert per group)
-        static const int reuse_env = [] {
-            const char* e = std::getenv("PNCE_TUNE_A_REUSE");
-            return e ? std::atoi(e) : 1;
-        }();
-        if (reuse_env == 1 && !narrow && !mid && tiling.n_groups > 1 && prm.k_blocks <= 64) {
+        if (kn.a_reuse == 1 && !narrow && !mid && tiling.n_groups > 1 && prm.k_blocks <= 64) {
             prm.a_reuse = 1;
-            const char* sp = std::getenv("PNCE_TUNE_SCR_POL");
-            prm.scr_pol = sp ? std::atoi(sp) : 1;
-            const char* ss = std::getenv("PNCE_TUNE_SCR_SLOTS");
-            prm.scr_slots = ss ? std::max(1, std::min(2, std::atoi(ss))) : 1;
+            prm.scr_pol = kn.scr_pol;
+            prm.scr_slots = kn.scr_slots > 0 ? std::max(1, std::min(2, kn.scr_slots)) : 1;
             prm.bar_bytes = 2048;
             budget -= 1024;
         }
         // scored drain: truth staged through a per-thread LDGSTS ring (8 epilogue warps x
         // slots x 2 KB) when the truth runs are 16-byte aligned (PNCE_TUNE_TRUTH_SLOTS, 0 = off)
-        static const int truth_slots_env = [] {
-            const char* e = std::getenv("PNCE_TUNE_TRUTH_SLOTS");
-            return e ? std::atoi(e) : 3;
-        }();
         if (scored && truth && (p->cfg.l % 2) == 0 && (reinterpret_cast<uintptr_t>(truth) & 15) == 0 &&
-            (prm.g_cols & 31) == 0 && truth_slots_env >= 2 && truth_slots_env <= 4) {
-            prm.truth_slots = truth_slots_env;
+            (prm.g_cols & 31) == 0 && kn.truth_slots >= 2 && kn.truth_slots <= 4) {
+            prm.truth_slots = kn.truth_slots;
             budget -= (int64_t)8 * prm.truth_slots * 2048;
         }
         int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
-        const char* as = std::getenv("PNCE_TUNE_AB_STAGES");
-        if (as) ab = std::min<int>((int)(budget / prm.stage_bytes), std::max(1, std::atoi(as)));
+        if (kn.ab_stages > 0) ab = std::min<int>((int)(budget / prm.stage_bytes), kn.ab_stages);
         int raw = (int)std::min<int64_t>(8, (budget - (int64_t)ab * prm.stage_bytes) / prm.raw_stage_bytes);
-        const char* rs = std::getenv("PNCE_TUNE_RAW_STAGES");
-        if (rs) raw = std::min(raw, std::max(1, std::atoi(rs)));
+        if (kn.raw_stages > 0) raw = std::min(raw, kn.raw_stages);
         if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
         prm.stages = ab;
         prm.raw_stages = raw;
@@ -2296,64 +2549,50 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
                                    (size_t)prm.raw_stages * prm.raw_stage_bytes);
         const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)8 * prm.truth_slots * 2048;
         const int grid = pair_grid(p, prm);
-        CUtensorMap tm_scr;
-        void* scratch = nullptr;
         if (prm.a_reuse) {
-            // [2 slots][clusters][2 CTAs][k_blocks] A stages of 128 rows x 128 B (stream-ordered
-            // allocation: the pool keeps it, so repeated launches do not reach the driver)
-            static std::once_flag pool_once;
-            std::call_once(pool_once, [] {
-                int dev = 0;
-                cudaMemPool_t pool;
-                if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                    uint64_t keep = UINT64_MAX;
-                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-                }
-            });
+            // [slots][clusters][2 CTAs][k_blocks] A stages of 128 rows x 128 B, owned by the
+            // (plan, stream) entry: allocated once, not per launch
             const uint64_t rows = (uint64_t)prm.scr_slots * (grid / 2) * 2 * prm.k_blocks * kBM;
-            cudaError_t e = cudaMallocAsync(&scratch, rows * 128, st);
-            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("A scratch: ") + cudaGetErrorString(e));
-            prm.scratch = static_cast<uint8_t*>(scratch);
-            s = make_tmap_scr(&tm_scr, scratch, rows);
-            if (s != PNCE_OK) {
-                cudaFreeAsync(scratch, st);
-                return s;
+            const uint8_t* before = res->scratch;
+            s_ok_or_return(ensure_buf(res->scratch, res->scratch_bytes, (size_t)rows * 128, st, "A scratch"));
+            if (res->scratch != before || res->tm_scr_rows != rows) {
+                s = make_tmap_scr(&res->tm_scr, res->scratch, rows);
+                if (s != PNCE_OK) {
+                    res->tm_scr_rows = 0;
+                    return s;
+                }
+                res->tm_scr_rows = rows;
             }
+            prm.scratch = res->scratch;
         }
         if (t16) {
             const int64_t n_fb = n_frames * p->n_batches;
-            uint32_t* flags = nullptr;
-            cudaError_t e = cudaMallocAsync(&flags, sizeof(uint32_t) * n_fb, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(flags, 0, sizeof(uint32_t) * n_fb, st);
-            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16 flags: ") + cudaGetErrorString(e));
+            s_ok_or_return(ensure_buf(res->flags, res->flags_n, (size_t)n_fb, st, "tensor16 flags"));
+            CUDA_TRY(cudaMemsetAsync(res->flags, 0, sizeof(uint32_t) * n_fb, st));
             prm.chunk_kb = t16->chunk_kb;
             prm.acc16 = t16->acc16;
-            prm.sat_flags = flags;
+            prm.sat_flags = res->flags;
             if (t16->acc16) prm.idesc &= ~(3u << 4);  // c_format = F16: binary16 partials in TMEM
             k_correlate<kModeFusedTma, false, false, true><<<grid, kThreadsK3, smem, st>>>(
-                tm_raw, p->t16.tm_circ, prm.a_reuse ? tm_scr : p->t16.tm_circ, prm);
+                res->tm_in, p->t16.tm_circ, prm.a_reuse ? res->tm_scr : p->t16.tm_circ, prm);
             g_launches++;
             const pnce_cfg_t& c = p->cfg;
-            k_t16_finish<<<(unsigned)n_fb, 256, 0, st>>>(taps, truth, stats, flags, c.n_r, c.n_t, c.n_batch,
+            k_t16_finish<<<(unsigned)n_fb, 256, 0, st>>>(taps, truth, stats, res->flags, c.n_r, c.n_t, c.n_batch,
                                                          p->n_batches, c.l);
-            e = cudaGetLastError();
-            cudaFreeAsync(flags, st);
-            if (e != cudaSuccess) return fail(PNCE_ERR_CUDA, std::string("tensor16: ") + cudaGetErrorString(e));
+            CUDA_TRY(cudaGetLastError());
         } else {
-            launch_k3<kModeFusedTma>(scored, grid, smem, st, tm_raw, tiling.tm_circ, prm,
-                                     prm.a_reuse ? &tm_scr : nullptr);
+            launch_k3<kModeFusedTma>(scored, grid, smem, st, res->tm_in, tiling.tm_circ, prm,
+                                     prm.a_reuse ? &res->tm_scr : nullptr);
         }
-        if (scratch) cudaFreeAsync(scratch, st);
     } else {
-        if (const char* as = std::getenv("PNCE_TUNE_AB_STAGES")) prm.stages = std::min(prm.stages, std::max(2, std::atoi(as)));
+        if (kn.ab_stages > 0) prm.stages = std::min(prm.stages, std::max(2, kn.ab_stages));
         const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         // the LDG variant reads the rows directly (tm_in unused; the circulant map fills the slot)
         launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, tiling.tm_circ, tiling.tm_circ, prm);
     }
-    diag_dump(st);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
+    if (scored && stats) s_ok_or_return(scored_finish(p, res, taps, truth, stats, link_err, n_frames, st));
+    diag_dump(st);
     return PNCE_OK;
 }
-
-

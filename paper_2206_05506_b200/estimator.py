@@ -6,7 +6,8 @@ Reference seam: `process_frames` (pnce/experiments.py:176-208) calling
 is a device plan (C ABI `pnce_plan_create`: device LFSR + stacked lag-window
 rows in tensor-core operand layout) and every frame-set goes through one device
 path: pack (CP strip, de-interleave, fp16/bf16) -> tcgen05 correlation -> fused
-1/M, demux and scoring.  There is no backend dispatch and no CPU fallback.
+1/M, demux and scoring.  There is no CPU fallback; the reference's BackendConfig
+selects between the fused path and its tensor16 mode (backend.py).
 """
 
 from __future__ import annotations
@@ -19,6 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .backend import resolve as resolve_backend
 from .errors import DimensionMismatchError, FrameTooShortError, InvalidConfigError
 from .pilots import BatchPlan, PilotConfig, build_batch_plan
 from .pn import LfsrSpec, PnSequence
@@ -30,8 +32,8 @@ DTYPES = {"fp16": _lib.PNCE_DTYPE_FP16, "bf16": _lib.PNCE_DTYPE_BF16}
 class CirEstimate:
     """estimator.py:27-37.  taps: complex64 device tensor (n_r, n_t, L) or (F, n_r, n_t, L).
 
-    ``stats`` (float64 (F, 4): sum|e|, sum|e|^2, non-finite count, 0) is filled
-    by the fused epilogue when ground truth was supplied, and ``link_mse``
+    ``stats`` (float64 (F, 4): sum|e|, sum|e|^2, non-finite taps, saturations) is filled
+    by the fused epilogue (the error sums when ground truth was supplied), and ``link_mse``
     (float32 (F, n_r, n_t) or (n_r, n_t)) with each link's mean |e|^2 over its L taps.
     """
 
@@ -71,6 +73,14 @@ def remove_cp(samples, c: int, m: int):
 
 def _stream_ptr(dev: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _same_device(dev: torch.device, **tensors) -> None:
+    """Every tensor argument must live on the plan's device: a foreign pointer would reach
+    TMA descriptors and kernels of another GPU (DimensionMismatchError instead)."""
+    for name, t in tensors.items():
+        if t is not None and (not t.is_cuda or t.device != dev):
+            raise DimensionMismatchError(f"{name} is on {t.device}, the correlator on {dev}")
 
 
 class Correlator:
@@ -133,6 +143,19 @@ class Correlator:
                                                   _stream_ptr(self.device)))
         return out
 
+    def operand(self) -> torch.Tensor:
+        """The plan's device-built correlation operand (fp16/bf16 [rows_alloc][K_pad], rows
+        j*L + l = chips shifted by s_j + l; batched_lag_rows, estimator.py:114-117)."""
+        L = _lib.lib()
+        rows, kp = ctypes.c_int32(), ctypes.c_int32()
+        _lib.check(L.pnce_plan_operand(self._plan, None, ctypes.byref(rows), ctypes.byref(kp), None))
+        tdt = torch.float16 if self.dtype == "fp16" else torch.bfloat16
+        out = torch.empty((rows.value, kp.value), dtype=tdt, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(L.pnce_plan_operand(self._plan, ctypes.c_void_p(out.data_ptr()), None, None,
+                                           _stream_ptr(self.device)))
+        return out
+
     def packed_bytes(self, n_frames: int) -> int:
         """Size of the packed 16-bit operand `pack` produces (the fused path needs none)."""
         return int(_lib.lib().pnce_workspace_bytes(self._plan, n_frames))
@@ -141,6 +164,7 @@ class Correlator:
     def _check_iq(self, iq: torch.Tensor) -> tuple[torch.Tensor, int]:
         if not isinstance(iq, torch.Tensor) or not iq.is_cuda:
             raise DimensionMismatchError("iq must be a CUDA tensor (use process_frames for host frames)")
+        _same_device(self.device, iq=iq)
         if iq.dtype != torch.float32:
             raise DimensionMismatchError(f"iq must be float32 (I, Q) pairs, got {iq.dtype}")
         if iq.dim() == 4:
@@ -179,9 +203,10 @@ class Correlator:
                 stats = torch.zeros((n_frames, 4), dtype=torch.float64, device=self.device)
         stats_ptr = None
         if stats is not None:
-            if tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64:
-                raise DimensionMismatchError("stats must be float64 (F, 4)")
+            if tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64 or not stats.is_contiguous():
+                raise DimensionMismatchError("stats must be contiguous float64 (F, 4)")
             stats_ptr = ctypes.c_void_p(stats.data_ptr())
+        _same_device(self.device, out=out, truth=truth, stats=stats)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().pnce_process_frames(
                 self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -210,6 +235,7 @@ class Correlator:
             link_mse = torch.zeros(lshape, dtype=torch.float32, device=self.device)
         elif tuple(link_mse.shape) != lshape or link_mse.dtype != torch.float32 or not link_mse.is_contiguous():
             raise DimensionMismatchError("link_mse must be contiguous float32 (F, n_r, n_t), zero-filled")
+        _same_device(self.device, out=out, truth=truth, stats=stats, link_mse=link_mse)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().pnce_process_frames_scored(
                 self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -239,8 +265,9 @@ class Correlator:
             truth_ptr = ctypes.c_void_p(truth.data_ptr())
         if stats is None:
             stats = torch.zeros((n_frames, 4), dtype=torch.float64, device=self.device)
-        elif tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64:
-            raise DimensionMismatchError("stats must be float64 (F, 4)")
+        elif tuple(stats.shape) != (n_frames, 4) or stats.dtype != torch.float64 or not stats.is_contiguous():
+            raise DimensionMismatchError("stats must be contiguous float64 (F, 4)")
+        _same_device(self.device, out=out, truth=truth, stats=stats)
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().pnce_process_frames_tensor16(
                 self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(out.data_ptr()), truth_ptr,
@@ -347,6 +374,7 @@ class Correlator:
     def correlate(self, packed: torch.Tensor, n_frames: int, truth: torch.Tensor | None = None,
                   out: torch.Tensor | None = None, stats: torch.Tensor | None = None):
         """K3+K4 alone on a packed operand."""
+        _same_device(self.device, packed=packed, out=out, truth=truth, stats=stats)
         if out is None:
             out = torch.empty(self.taps_shape(n_frames), dtype=torch.complex64, device=self.device)
         truth_ptr = ctypes.c_void_p(truth.data_ptr()) if truth is not None else None
@@ -391,7 +419,7 @@ def _frames_to_iq(frames, cfg: PilotConfig) -> np.ndarray:
     return iq
 
 
-def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, backend: str | None = None,
+def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, backend=None,
                    counters: WorkCounters | None = None, rows_per_batch: Correlator | None = None,
                    truth=None) -> CirEstimate:
     """experiments.py:176-208 on the device: CP removal, correlation, demux, 1/M.
@@ -399,11 +427,15 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
     ``frames``: either the reference's per-batch list of (n_r, P+L-1) complex
     frames (host; copied to the device as f32 IQ) or a CUDA float32 IQ tensor
     (n_batches, n_r, P+L-1, 2) / (F, n_batches, n_r, P+L-1, 2).
-    ``backend``: operand precision "fp16" (default) or "bf16" -- the single
-    device path has no reference64/32 branches.  ``rows_per_batch``: a prebuilt
-    Correlator (the static state the reference passes as rows_per_batch).
+    ``backend``: the reference's ``BackendConfig`` (ours in backend.py or pnce's own):
+    reference64 / reference32 run the fused fp16 path, tensor16 runs the tensor16 mode
+    with its chunk_len / accumulator (backend.py has the mapping and tolerances); or
+    "fp16" / "bf16" for the fused path at that operand precision.  ``rows_per_batch``: a
+    prebuilt Correlator (the static state the reference passes as rows_per_batch).
+    A saturated (frame-set, batch) is scored as all-zero taps and counted as n_r * n_tx
+    saturations, as the reference does (experiments.py:201-205).
     """
-    dtype = backend or (rows_per_batch.dtype if rows_per_batch is not None else "fp16")
+    mode = resolve_backend(backend, rows_per_batch.dtype if rows_per_batch is not None else None)
     single = True
     if isinstance(frames, torch.Tensor):
         iq = frames
@@ -414,8 +446,8 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
         n_r = host.shape[2]
         iq = torch.from_numpy(host).to(seq.chips.device, non_blocking=False)
     corr = rows_per_batch
-    if corr is None or corr.n_r != n_r or corr.dtype != dtype or corr.cfg != cfg:
-        corr = correlator_rows_for_plan(seq, plan, cfg, n_r, dtype)
+    if corr is None or corr.n_r != n_r or corr.dtype != mode.dtype or corr.cfg != cfg:
+        corr = correlator_rows_for_plan(seq, plan, cfg, n_r, mode.dtype)
     truth_t = None
     if truth is not None:
         tt = getattr(truth, "taps", truth)
@@ -423,20 +455,23 @@ def process_frames(seq: PnSequence, cfg: PilotConfig, plan: BatchPlan, frames, b
         truth_t = truth_t.to(device=corr.device, dtype=torch.complex64)
         if truth_t.dim() == 3:
             truth_t = truth_t.unsqueeze(0)
+    n_frames = 1 if single else int(iq.shape[0])
+    # stats always: the saturation count (stats[:, 3]) comes with them
+    stats = torch.zeros((n_frames, 4), dtype=torch.float64, device=corr.device)
     link_mse = None
-    if truth_t is not None:
-        taps, stats, link_mse = corr.process_scored(iq, truth_t)
+    if mode.tensor16:
+        taps, stats = corr.process_tensor16(iq, chunk_len=mode.chunk_len, accumulator=mode.accumulator,
+                                            truth=truth_t, stats=stats)
+    elif truth_t is not None:
+        taps, stats, link_mse = corr.process_scored(iq, truth_t, stats=stats)
     else:
-        taps, stats = corr.process(iq)
-    n_frames = taps.shape[0]
+        taps, stats = corr.process(iq, stats=stats)
     if counters is not None:
         counters.samples_moved += n_frames * cfg.n_batches * n_r * cfg.p
         counters.macs += n_frames * cfg.n_t * cfg.l * cfg.m * n_r
     out_taps = taps[0] if single else taps
-    saturations = 0
-    if stats is not None:
-        saturations = int(stats[:, 2].sum().item())
+    saturations = int(round(float(stats[:, 3].sum().item())))
     if link_mse is not None and single:
         link_mse = link_mse[0]
-    return CirEstimate(taps=out_taps, backend=f"tcgen05-{dtype}", norm=1.0 / cfg.m,
-                       saturations=saturations, stats=stats, link_mse=link_mse)
+    return CirEstimate(taps=out_taps, backend=mode.kind, norm=1.0 / cfg.m, saturations=saturations,
+                       stats=stats if truth_t is not None else None, link_mse=link_mse)

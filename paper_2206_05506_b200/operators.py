@@ -6,7 +6,9 @@ rows plan (`pnce_plan_create_rows`: fp16/bf16 K-major operand of the given rows,
 scale) and correlates the received columns as compact body rows (`pnce_process_bodies`).
 `RowsCorrelator` keeps the plan for repeated use with the same rows.  The single device
 path computes with fp16 (default) or bf16 operands and fp32 accumulation -- the
-reference's tensor16 quantiser; there is no reference64/32 branch.
+reference's tensor16 quantiser; the reference's ``BackendConfig`` is accepted (backend.py):
+reference64/32 run that path, tensor16 runs the chunked tensor16 mode and raises
+SaturationDetectedError like halfprec.py:118-124.
 """
 
 from __future__ import annotations
@@ -18,7 +20,9 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import DimensionMismatchError, InvalidConfigError, PlanMismatchError, RowsOutOfRangeError
+from .backend import resolve as resolve_backend
+from .errors import (DimensionMismatchError, InvalidConfigError, PlanMismatchError, RowsOutOfRangeError,
+                     SaturationDetectedError)
 from .estimator import DTYPES, _stream_ptr
 from .pilots import BatchAssignment, cyclic_separation
 from .pn import PnSequence
@@ -60,8 +64,9 @@ class RowsCorrelator:
                 pass
             self._plan = None
 
-    def __call__(self, y) -> torch.Tensor:
-        """y: (M,) or (M, cols) complex -> (R,) or (R, cols) complex64 on the device."""
+    def __call__(self, y, tensor16: tuple | None = None) -> torch.Tensor:
+        """y: (M,) or (M, cols) complex -> (R,) or (R, cols) complex64 on the device.
+        ``tensor16``: (chunk_len | None, accumulator) runs the tensor16 mode."""
         yt = y if isinstance(y, torch.Tensor) else torch.from_numpy(np.asarray(y, dtype=np.complex128))
         squeeze = yt.dim() == 1
         y2 = yt[:, None] if squeeze else yt
@@ -75,19 +80,31 @@ class RowsCorrelator:
         body[:, :self.m] = torch.view_as_real(yc.contiguous())
         taps = torch.empty((1, self.cols, 1, self.n_rows), dtype=torch.complex64, device=self.device)
         with torch.cuda.device(self.device):
-            _lib.check(_lib.lib().pnce_process_bodies(self._plan, ctypes.c_void_p(body.data_ptr()), self.stride,
-                                                      ctypes.c_void_p(taps.data_ptr()), None, None, None, 1,
-                                                      _stream_ptr(self.device)))
+            if tensor16 is not None:
+                chunk_len, acc = tensor16
+                stats = torch.zeros((1, 4), dtype=torch.float64, device=self.device)
+                _lib.check(_lib.lib().pnce_process_bodies_tensor16(
+                    self._plan, ctypes.c_void_p(body.data_ptr()), self.stride, ctypes.c_void_p(taps.data_ptr()),
+                    None, ctypes.c_void_p(stats.data_ptr()), 0 if chunk_len is None else int(chunk_len),
+                    1 if acc == "binary16" else 0, 1, _stream_ptr(self.device)))
+                if float(stats[0, 3].item()) > 0:
+                    raise SaturationDetectedError(f"non-finite {acc} partial or running total")
+            else:
+                _lib.check(_lib.lib().pnce_process_bodies(self._plan, ctypes.c_void_p(body.data_ptr()), self.stride,
+                                                          ctypes.c_void_p(taps.data_ptr()), None, None, None, 1,
+                                                          _stream_ptr(self.device)))
         out = taps[0, :, 0, :].transpose(0, 1)                       # (R, cols)
         return out[:, 0] if squeeze else out
 
 
-def correlate_rows(rows, y, backend: str | None = None, norm_len: int | None = None) -> torch.Tensor:
+def correlate_rows(rows, y, backend=None, norm_len: int | None = None) -> torch.Tensor:
     """estimator.py:68-86: (1/norm_len) rows @ y for complex y ((M,) or (M, cols)).
-    ``backend``: operand dtype "fp16" (default) or "bf16"."""
+    ``backend``: the reference's BackendConfig (backend.py mapping) or "fp16" (default) / "bf16"."""
+    mode = resolve_backend(backend)
     yt = y if isinstance(y, torch.Tensor) else np.asarray(y)
     cols = 1 if yt.ndim == 1 else int(yt.shape[1])
-    return RowsCorrelator(rows, cols, norm_len, dtype=backend or "fp16")(y)
+    corr = RowsCorrelator(rows, cols, norm_len, dtype=mode.dtype)
+    return corr(y, (mode.chunk_len, mode.accumulator) if mode.tensor16 else None)
 
 
 def _lag_rows(seq: PnSequence, lags) -> torch.Tensor:

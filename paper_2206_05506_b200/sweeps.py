@@ -8,9 +8,14 @@ MAE scoring by the fused correlator -- and the points of a grid distributed roun
 over the ranks of a process group (NCCL/gloo), gathered in grid order on rank 0.
 
 Per point and iteration the (channel, noise) seeds derive from the master seed and the
-grid key exactly as the reference does (numpy SeedSequence, experiments.py:151-154);
-they seed Philox streams, so MAE values are statistically -- not draw-for-draw --
-equivalent.  `latency_s` is the device time per frame-set of the fused scored kernel.
+grid key exactly as the reference does (numpy SeedSequence, experiments.py:151-154).
+By default they seed the device synthesiser's Philox streams, so MAE values are
+statistically -- not draw-for-draw -- equivalent.  With a ``frame_source`` (the
+reference's own `simulate_frame` output for those seeds: a host callable returning
+(truth taps, per-batch frames), experiments.py:217-231) every iteration estimates exactly
+the frames the reference would, so the curves match the reference's draw for draw; the
+frames are quantised to f32 I/Q as the IQ-file writer does (iqfile.py:86-89).
+`latency_s` is the device time per frame-set of the fused scored kernel.
 """
 
 from __future__ import annotations
@@ -190,26 +195,53 @@ def _correlator(cfg: ExperimentConfig, m: int, n_batch: int, device: torch.devic
     return _CORR_CACHE[key]
 
 
-def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device) -> list[SweepResult]:
-    """_sweep_point (experiments.py:234-296) on the device: all iterations as one batch."""
+def _host_frames(frame_source, corr, pt: SweepPoint, seeds) -> tuple[torch.Tensor, torch.Tensor]:
+    """Frames of every iteration from a host frame source -> pinned (truth c64, iq f32)."""
+    import numpy as np
+    from .estimator import _frames_to_iq
+    it_n = len(seeds)
+    h = torch.empty(corr.taps_shape(it_n), dtype=torch.complex64).pin_memory()
+    iq = torch.empty(corr.iq_shape(it_n), dtype=torch.float32).pin_memory()
+    for it, (cs, ns) in enumerate(seeds):
+        truth, frames = frame_source(corr.cfg, corr.n_r, pt.l_nz, pt.snr_db, cs, ns)
+        truth = np.asarray(getattr(truth, "taps", truth))
+        if truth.shape != tuple(corr.taps_shape(1)[1:]):
+            raise SchemaMismatchError(f"frame source truth shape {truth.shape} != {corr.taps_shape(1)[1:]}")
+        h[it] = torch.from_numpy(truth.astype(np.complex64))
+        iq[it] = torch.from_numpy(_frames_to_iq(frames, corr.cfg)[0])
+    return h, iq
+
+
+def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device,
+                   frame_source=None) -> list[SweepResult]:
+    """_sweep_point (experiments.py:234-296) on the device: all iterations as one batch.
+
+    ``frame_source(pilot, n_r, l_nz, snr_db, chan_seed, noise_seed) -> (truth, frames)``:
+    host frames instead of the device synthesiser (see the module docstring)."""
     from . import synth
     corr = _correlator(cfg, pt.m, pt.n_batch, device)
     it_n = cfg.iterations
     seeds = [derive_seeds(cfg.seed, pt.m, pt.n_batch, pt.l_nz, pt.si, it) for it in range(it_n)]
-    h = torch.empty(corr.taps_shape(it_n), dtype=torch.complex64, device=device)
-    iq = torch.empty(corr.iq_shape(it_n), dtype=torch.float32, device=device)
-    for it, (cs, ns) in enumerate(seeds):
-        h[it:it + 1] = synth.draw_channel(corr, 1, l_nz=pt.l_nz, seed=cs)
-        synth.simulate_frames(corr, h[it:it + 1], pt.snr_db, seed=ns, out=iq[it:it + 1])
+    if frame_source is not None:
+        h_host, iq_host = _host_frames(frame_source, corr, pt, seeds)
+        h = h_host.to(device, non_blocking=True)
+        iq = iq_host.to(device, non_blocking=True)
+    else:
+        h = torch.empty(corr.taps_shape(it_n), dtype=torch.complex64, device=device)
+        iq = torch.empty(corr.iq_shape(it_n), dtype=torch.float32, device=device)
+        for it, (cs, ns) in enumerate(seeds):
+            h[it:it + 1] = synth.draw_channel(corr, 1, l_nz=pt.l_nz, seed=cs)
+            synth.simulate_frames(corr, h[it:it + 1], pt.snr_db, seed=ns, out=iq[it:it + 1])
+    stream = torch.cuda.current_stream(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    ev0.record(stream)
     _, stats, _ = corr.process_scored(iq, h)
-    ev1.record()
+    ev1.record(stream)
     torch.cuda.synchronize(device)
     per_frame = (ev0.elapsed_time(ev1) / 1e3) / it_n if cfg.record_latency else 0.0
     n_taps = cfg.n_r * cfg.n_t * cfg.l
     maes = (stats[:, 0] / n_taps).tolist()
-    sats = stats[:, 2].round().long().tolist()
+    sats = stats[:, 3].round().long().tolist()   # n_r * n_tx per saturated batch (experiments.py:201-205)
     pil = corr.cfg
     samples_moved = pil.n_batches * cfg.n_r * pil.p
     macs = cfg.n_t * cfg.l * pt.m * cfg.n_r
@@ -225,24 +257,25 @@ def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device) 
     return rows
 
 
-def _run(cfg: ExperimentConfig, points: Sequence[SweepPoint], device=None, group=None) -> list[SweepResult] | None:
+def _run(cfg: ExperimentConfig, points: Sequence[SweepPoint], device=None, group=None,
+         frame_source=None) -> list[SweepResult] | None:
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     if device is None:
         device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
-    mine = [(i, evaluate_point(cfg, pt, device)) for i, pt in shard(points, rank, world)]
+    mine = [(i, evaluate_point(cfg, pt, device, frame_source)) for i, pt in shard(points, rank, world)]
     return _gather_rows(mine, group)
 
 
-def run_snr_sweep(cfg: ExperimentConfig, device=None, group=None) -> list[SweepResult] | None:
+def run_snr_sweep(cfg: ExperimentConfig, device=None, group=None, frame_source=None) -> list[SweepResult] | None:
     """MAE vs SNR over the (PN length, N_batch) grid; rows on rank 0 (None elsewhere)."""
-    return _run(cfg, snr_sweep_points(cfg), device, group)
+    return _run(cfg, snr_sweep_points(cfg), device, group, frame_source)
 
 
-def run_tap_sweep(cfg: ExperimentConfig, device=None, group=None) -> list[SweepResult] | None:
+def run_tap_sweep(cfg: ExperimentConfig, device=None, group=None, frame_source=None) -> list[SweepResult] | None:
     """MAE vs SNR while varying the tap count (M, N_batch fixed to the grid heads)."""
-    return _run(cfg, tap_sweep_points(cfg), device, group)
+    return _run(cfg, tap_sweep_points(cfg), device, group, frame_source)
 
 
 @dataclass
@@ -294,9 +327,9 @@ def run_latency_bench(cfg: ExperimentConfig, reps: int = 10, warmup: int = 2, de
             times = []
             for rep in range(warmup + reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
+                e0.record(torch.cuda.current_stream(device))
                 corr.process(iq, out=taps)
-                e1.record()
+                e1.record(torch.cuda.current_stream(device))
                 torch.cuda.synchronize(device)
                 if rep >= warmup:
                     times.append(e0.elapsed_time(e1) / 1e3)

@@ -204,14 +204,16 @@ def test_errors_map_to_reference_classes(dev):
 
 
 def test_nonfinite_counted_not_raised(dev):
-    """experiments.py:201-205 counts saturation instead of aborting: inf input -> counted taps."""
+    """experiments.py:201-205 counts saturation instead of aborting: inf input -> the batch
+    (4 receivers x 1 transmitter) is zeroed and counted as n_r * n_tx = 4 saturations."""
     cfg, ocfg = make_cfg(4, 127, 16, 1)
     _, iq, truth = sim_sets(ocfg, 1)
     iq[0, 0, 0, 20, 0] = np.inf
     corr = P.Correlator(P.default_spec(7), cfg, 4, device=dev)
-    _, stats = corr.process(torch.from_numpy(iq).to(dev),
-                            truth=torch.from_numpy(truth.astype(np.complex64)).to(dev))
-    assert stats[0, 2].item() > 0
+    taps, stats = corr.process(torch.from_numpy(iq).to(dev),
+                               truth=torch.from_numpy(truth.astype(np.complex64)).to(dev))
+    assert stats[0, 3].item() == 4 and stats[0, 2].item() == 0
+    assert (taps[0, :, 0] == 0).all() and torch.isfinite(torch.view_as_real(taps)).all()
 
 
 def test_snr_curve_within_01db(dev, golden):

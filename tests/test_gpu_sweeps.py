@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+from oracle import pnce_oracle as O
 from paper_2206_05506_b200 import sweeps as SW
 
 pytestmark = pytest.mark.gpu
@@ -18,6 +19,55 @@ def dev():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+def oracle_source(pilot, n_r, l_nz, snr_db, chan_seed, noise_seed):
+    """The reference's simulate_frame for these seeds (oracle restatement, pinned to the
+    reference's IQ bytes by test_oracle.py)."""
+    ocfg = O.Config(m=pilot.m, c=pilot.c, n_t=pilot.n_t, n_batch=pilot.n_batch, l=pilot.l, n_r=n_r)
+    return O.simulate_frame(O.sequence_for_length(pilot.m), ocfg, l_nz, snr_db, chan_seed, noise_seed)
+
+
+def db(a, b):
+    return abs(10 * math.log10(a / b))
+
+
+def test_snr_sweep_identical_inputs_match_reference_csv(dev):
+    """With the reference's own frames (frame_source) every row matches the reference's
+    run_snr_sweep CSV: counters exactly, MAE within 0.01 dB (draw for draw)."""
+    with open(os.path.join(GOLD, "ref_snr_sweep.csv"), newline="") as fh:
+        ref = SW.parse_csv(fh.read())
+    cfg = SW.ExperimentConfig(n_t=4, n_r=4, pn_lengths=(63, 127), c=16, l=16, l_nz=(16,), n_batch=(1,),
+                              snr_db=(-10.0, 10.0, 30.0), iterations=4, seed=0, record_latency=False)
+    rows = SW.run_snr_sweep(cfg, device=dev, frame_source=oracle_source)
+    assert len(rows) == len(ref)
+    for a, b in zip(rows, ref):
+        assert (a.m, a.snr_db, a.samples_moved, a.macs, a.saturations) == (b.m, b.snr_db, b.samples_moved, b.macs,
+                                                                          b.saturations)
+        assert db(a.mae, b.mae) <= 0.01, (a, b)
+
+
+def test_table1_grid_draw_for_draw(dev):
+    """The paper's Table I grid at cfg2 (SNR 0..30 dB step 5 x 50 iterations, seed 0) on the
+    reference's own frames: every per-iteration MAE within 0.05 dB and every point within
+    0.01 dB of the REAL reference's sweep (tests/golden/ref_cfg2_table1.csv)."""
+    with open(os.path.join(GOLD, "ref_cfg2_table1.csv"), newline="") as fh:
+        ref = SW.parse_csv(fh.read())
+    cfg = SW.ExperimentConfig(n_t=16, n_r=16, pn_lengths=(255,), c=32, l=32, l_nz=(32,), n_batch=(4,),
+                              snr_db=tuple(float(s) for s in range(0, 31, 5)), iterations=50, seed=0,
+                              emit_per_iteration=True, record_latency=False)
+    rows = SW.run_snr_sweep(cfg, device=dev, frame_source=oracle_source)
+    assert len(rows) == len(ref) == 7 * 51
+    worst_it = worst_pt = 0.0
+    for a, b in zip(rows, ref):
+        assert (a.experiment, a.snr_db, a.iterations, a.seed, a.samples_moved, a.macs, a.saturations) == \
+               (b.experiment, b.snr_db, b.iterations, b.seed, b.samples_moved, b.macs, b.saturations)
+        d = db(a.mae, b.mae)
+        if a.experiment == "snr_sweep":
+            worst_pt = max(worst_pt, d)
+        else:
+            worst_it = max(worst_it, d)
+    assert worst_pt <= 0.01 and worst_it <= 0.05, (worst_pt, worst_it)
 
 
 def test_snr_sweep_rows_match_reference_csv(dev):
