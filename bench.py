@@ -284,6 +284,44 @@ def cfg4_leg(P, S, dev, stream, F4, steps, tf_burst, tf_sust):
     return out
 
 
+def antenna_leg(P, D, dev, stream, w, iq1, reps, rank, world):
+    """One cfg3 frame-set split over the ranks by receive antenna, the paper's scheme
+    (PAPER.md:150-153): each rank estimates its N_r / N_ranks receivers in one fused launch,
+    then the CIRs are all-gathered so every rank holds the full CSI.  Per rep: barrier, CUDA
+    events on the launching stream around the launch (kernel) and around launch + all-gather
+    (total); each figure is the max over ranks, then the median over reps."""
+    import statistics as st
+
+    import torch
+    import torch.distributed as dist
+    r0, r1 = D.antenna_shard(w["n_r"], rank, world)
+    cfg = P.PilotConfig(m=w["m"], c=w["c"], n_t=w["n_t"], n_batch=w["n_batch"], l=w["l"], f_s=10e6)
+    part = P.Correlator(P.default_spec(10), cfg, r1 - r0, device=dev)
+    iq_r = iq1[:, :, r0:r1].contiguous()
+    taps_r = torch.empty(part.taps_shape(1), dtype=torch.complex64, device=dev)
+    kern, tot = [], []
+    for i in range(reps + 5):
+        if world > 1:
+            dist.barrier()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        part.process(iq_r, out=taps_r)
+        e1.record(stream)
+        csi = D.allgather_csi(taps_r)
+        e2.record(stream)
+        torch.cuda.synchronize(dev)
+        k, t = D.max_over_ranks([e0.elapsed_time(e1) * 1e3, e0.elapsed_time(e2) * 1e3])
+        if i >= 5:
+            kern.append(k)
+            tot.append(t)
+    assert csi.shape == (1, w["n_r"], w["n_t"], w["l"])
+    return {"ranks": world, "receivers_per_rank": r1 - r0, "frames": 1, "reps": reps,
+            "kernel_us_median": st.median(kern), "with_allgather_us_median": st.median(tot),
+            "allgather_bytes": w["n_r"] * w["n_t"] * w["l"] * 8,
+            "note": "per rep: max over ranks of CUDA-event time (launch; launch + all-gather of the CIRs)"}
+
+
 def run_gpu(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -292,7 +330,9 @@ def run_gpu(args, rank, world):
     from paper_2206_05506_b200 import _lib
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = torch.device("cuda", local)
+    # one process per GPU; with more ranks than GPUs (a gloo smoke run of the multi-rank
+    # path on a 1-GPU box) ranks share devices round-robin
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     w = dict(WORKLOAD)
     F = args.frames
@@ -330,7 +370,7 @@ def run_gpu(args, rank, world):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.25)
     launches0 = L.pnce_kernel_launches()
@@ -346,10 +386,9 @@ def run_gpu(args, rank, world):
     t_total = evs[0].elapsed_time(evs[-1]) / 1e3                      # s, device time
     t_step = [evs[i].elapsed_time(evs[i + 1]) / 1e3 for i in range(args.steps)]
     t_kernel = sum(t_step) / args.steps                                # one launch per step
+    from paper_2206_05506_b200 import distributed as D
     if world > 1:
-        t = torch.tensor([t_total, t_kernel], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total, t_kernel = (float(x) for x in t.tolist())
+        t_total, t_kernel = D.max_over_ranks([t_total, t_kernel])
     ms_per_step = t_total / args.steps * 1e3
     frames_total = F * world
     frames_per_s = frames_total * args.steps / t_total
@@ -372,7 +411,6 @@ def run_gpu(args, rank, world):
 
     # --- estimate quality on the synthetic input: fused scoring + NCCL all-reduce of the
     # per-rank error sums (the only collective of the path)
-    from paper_2206_05506_b200 import distributed as D
     quality = None
     if not args.no_quality:
         # fused scoring (taps + per-frame sums + per-link MSE) over the first Fq frame-sets
@@ -488,6 +526,11 @@ def run_gpu(args, rank, world):
                "note": "device: one fused launch on one resident cfg3 frame-set (4 CTA pairs busy); "
                        "e2e: pinned host IQ -> H2D (CP stripped in the DMA) -> kernel -> D2H taps, wall clock"}
 
+    # --- the paper's multi-GPU split of one frame-set: receivers over ranks + CSI all-gather
+    ant = None
+    if args.antenna_reps > 0:
+        ant = antenna_leg(P, D, dev, stream, w, iq[:1], args.antenna_reps, rank, world)
+
     # --- BASELINE configs[3] (cfg4', tensor-bound): fused and packed-GEMM tensor fractions
     c4 = None
     if args.cfg4_frames > 0:
@@ -515,9 +558,7 @@ def run_gpu(args, rank, world):
         torch.cuda.synchronize(dev)
         te = t0.elapsed_time(t1) / 1e3
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+            te = D.max_over_ranks([te])[0]
         e2e = {"value": Fe * world * reps / te * w["n_r"] * w["n_t"], "unit": "CSI estimates/s",
                "h2d_bytes_per_step": Fe * corr.cfg.n_batches * w["n_r"] * w["m"] * 8,   # body-only pitched DMA
                "d2h_bytes_per_step": host_taps.numel() * 8,
@@ -552,7 +593,9 @@ def run_gpu(args, rank, world):
             "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8 (BASELINE configs[2])",
                        "frames_per_step": F, "input_bytes_per_step": iq.numel() * 4,
                        "l2": "inputs (47 GB f32 IQ at 10k frames) >> 126 MB L2; no flush needed",
-                       "parallelism": f"dp{world} (frames sharded, no hot-path collective)"},
+                       "parallelism": f"dp{world} (frames sharded, no hot-path collective)",
+                       "dist_backend": args.dist_backend if world > 1 else None,
+                       "distinct_devices": min(world, torch.cuda.device_count())},
             "tensor_pct_of_peak": 100 * achieved_tf / tf_burst,
             "kernels": {"k_correlate_fused_ms": t_kernel * 1e3, "tflops": achieved_tf, "gbs": achieved_gbs},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
@@ -568,6 +611,7 @@ def run_gpu(args, rank, world):
             "tensor16_leg": t16,
             "cfg4_leg": c4,
             "latency": lat,
+            "antenna_split": ant,
             "cpu_baseline": cpu, "e2e": e2e, "ingest_iq_file": ingest, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -595,6 +639,9 @@ def main():
     ap.add_argument("--latency-reps", type=int, default=50, help="single frame-set latency samples (0: off)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend under torchrun (gloo: several ranks may share one GPU)")
+    ap.add_argument("--antenna-reps", type=int, default=50, help="antenna-sharded latency samples (0: off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -605,8 +652,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+        dist.init_process_group(args.dist_backend)
     try:
         return run_gpu(args, rank, world)
     finally:
