@@ -1813,6 +1813,10 @@ PlanView plan_view(const pnce_plan_t* p) {
 }
 pnce_status_t set_error(pnce_status_t code, const std::string& msg) { return fail(code, msg); }
 void count_launch() { g_launches++; }
+pnce_status_t encode_tmap_k16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                              int bf16) {
+    return make_tmap(map, base, cols, rows, box_rows, bf16);
+}
 }  // namespace pnce_internal
 
 static pnce_status_t device_setup(int dev);

@@ -15,11 +15,15 @@
 //
 // The body n in [C, C+M) is the circular convolution, i.e. the GEMM
 //   Y[(plane, f, r), k] = H[(plane, f, r), (j, l)] . A[(j, l), k],  A = chip[(k - s_j - l) mod M]
-// (the same lag-window rows the correlator uses; +-1 exact), done with cuBLAS SGEMM (a plain
-// library GEMM, fp32).  The cyclic prefix is the body's tail and the convolution tail its
-// head, minus the few terms that fall outside the pilot: y[n < C] = Y[n + M - C] -
+// (the same lag-window rows the correlator uses; +-1 exact), done on the tensor cores by
+// k_synth_gemm (tcgen05 kind::f16 with bf16 operands, fp32 accumulator in TMEM): H is split
+// into three bf16 terms h = b0 + b1 + b2 (24 mantissa bits, fp32's exponent range, so no
+// scaling), A is +-1 (exact in bf16), the products are exact and the sums fp32 -- the
+// accuracy of an fp32 SGEMM.  The cyclic prefix is the body's tail and the convolution tail
+// its head, minus the few terms that fall outside the pilot: y[n < C] = Y[n + M - C] -
 // sum_{l > n} ..., y[P + q] = Y[q] - sum_{l <= q} ... (at most L - 1 terms each).
-#include <cublas_v2.h>
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
 
@@ -27,11 +31,15 @@
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/pnce_b200.h"
 #include "pnce_internal.h"
+#include "sm100_ptx.cuh"
 
 namespace {
+
+using namespace pnce;
 
 using pnce_internal::PlanView;
 
@@ -76,25 +84,139 @@ __global__ void k_draw_channel(float2* __restrict__ h, int64_t n_links, int L, i
 
 constexpr int kSynThreads = 256;
 
-// A[(j, l), k] = chip[(k - s_j - l) mod M] as fp32, rows = n_batch * L
-__global__ void k_build_a32(const float* __restrict__ chips, float* __restrict__ a, int m, int l, int rows,
-                            int spacing) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)rows * m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int row = (int)(i / m), k = (int)(i - (int64_t)row * m);
-        const int j = row / l, lag = row - j * l;
-        int idx = (k - spacing * j - lag) % m;
-        if (idx < 0) idx += m;
-        a[i] = chips[idx];
+// ---------------------------------------------------------------- tensor-core body GEMM
+// Y[row, k] = sum_q Hs[row, q] Bs[k, q] with K' = 3 * Rp (Rp = roundup(n_batch L, 64)):
+//   Hs[row][t * Rp + (j L + l)] = b_t(h[f, r, b*n_batch + j, l]) (plane re/im by row half),
+//   Bs[k][t * Rp + (j L + l)]  = chip[(k - s_j - l) mod M]       (t = 0, 1, 2)
+// so the three bf16 terms of h meet the same +-1 entry.  One CTA per 128 x 256 tile of Y:
+// warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one thread), warps 2-5 epilogue.
+constexpr int kSgM = 128, kSgN = 256, kSgK = 64, kSgStages = 4;
+constexpr uint32_t kSgABytes = kSgM * kSgK * 2, kSgBBytes = kSgN * kSgK * 2;
+constexpr uint32_t kSgStageBytes = kSgABytes + kSgBBytes;
+constexpr int kSgThreads = 192;
+
+// Bs [Np][3 Rp] bf16 (Np = roundup(M, 256)), zero outside k < M, q < n_batch L
+__global__ void k_build_bsyn(const float* __restrict__ chips, __nv_bfloat16* __restrict__ bs, int m, int l, int nbl,
+                             int rp, int np, int spacing) {
+    const int64_t total = (int64_t)np * 3 * rp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i / (3 * rp));
+        const int q = (int)(i - (int64_t)k * 3 * rp) % rp;
+        float v = 0.f;
+        if (k < m && q < nbl) {
+            const int j = q / l, lag = q - j * l;
+            int idx = (k - spacing * j - lag) % m;
+            if (idx < 0) idx += m;
+            v = chips[idx];
+        }
+        bs[i] = __float2bfloat16_rn(v);
     }
 }
 
-// h complex64 [F][n_r][n_t][L] -> planes [2][F][n_r][n_t][L] (re, im)
-__global__ void k_h_planes(const float2* __restrict__ h, float* __restrict__ hp, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float2 v = h[i];
-        hp[i] = v.x;
-        hp[n + i] = v.y;
+// Hs rows (plane, f, r) of batch b: the three bf16 terms of each tap, zero beyond n_tx L
+__global__ void k_h_split(const float2* __restrict__ h, __nv_bfloat16* __restrict__ hs, int64_t fr, int n_t, int l,
+                          int b, int n_batch, int n_tx, int rp) {
+    const int64_t total = 2 * fr * rp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / rp;
+        const int q = (int)(i - row * rp);
+        const int plane = row >= fr;
+        const int64_t link = plane ? row - fr : row;   // f * n_r + r
+        float x = 0.f;
+        if (q < n_tx * l) {
+            const float2 v = h[(link * n_t + (int64_t)b * n_batch) * l + q];
+            x = plane ? v.y : v.x;
+        }
+        const __nv_bfloat16 b0 = __float2bfloat16_rn(x);
+        const float r0 = x - __bfloat162float(b0);
+        const __nv_bfloat16 b1 = __float2bfloat16_rn(r0);
+        const __nv_bfloat16 b2 = __float2bfloat16_rn(r0 - __bfloat162float(b1));
+        __nv_bfloat16* dst = hs + row * 3 * rp + q;
+        dst[0] = b0;
+        dst[rp] = b1;
+        dst[2 * rp] = b2;
+    }
+}
+
+__global__ void __launch_bounds__(kSgThreads, 1)
+k_synth_gemm(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_b,
+             float* __restrict__ y, int64_t rows, int m, int k_blocks) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSgStages * kSgStageBytes);
+    uint64_t* empty = full + kSgStages;
+    uint64_t* done = empty + kSgStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * kSgM;
+    const int col0 = blockIdx.y * kSgN;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSgStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tslot, kSgN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_h);
+        tma_prefetch(&tm_b);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+            const int s = kb % kSgStages;
+            mbar_wait(&empty[s], ((kb / kSgStages) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[s], kSgStageBytes);
+            uint8_t* sa = smem + s * kSgStageBytes;
+            tma_load_2d(sa, &tm_h, &full[s], kb * kSgK, (int)row0, policy_evict_first());
+            tma_load_2d(sa + kSgABytes, &tm_b, &full[s], kb * kSgK, col0, policy_evict_last());
+        }
+    } else if (warp == 1 && lane == 0) {
+        const uint32_t idesc = make_idesc_f16(kSgM, kSgN, 1);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+            const int s = kb % kSgStages;
+            mbar_wait(&full[s], (kb / kSgStages) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * kSgStageBytes);
+#pragma unroll
+            for (int ks = 0; ks < kSgK / 16; ++ks)
+                umma_f16_ss(tmem, make_sdesc(sa + ks * 32, 16, 1024, 2),
+                            make_sdesc(sa + kSgABytes + ks * 32, 16, 1024, 2), idesc, (kb | ks) != 0);
+            umma_commit(&empty[s]);
+        }
+        umma_commit(done);
+    } else if (warp >= 2) {
+        // warp w drains TMEM lanes 32 (w % 4) .. +31 (its sub-partition): one Y row per thread
+        const int q = warp & 3;
+        mbar_wait(done, 0);
+        tc_fence_after();
+        const int64_t row = row0 + q * 32 + lane;
+        float* dst = y + row * (int64_t)m + col0;
+        const bool vec = (m & 3) == 0;
+        for (int c = 0; c < kSgN; c += 32) {
+            uint32_t v[32];
+            tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+            tmem_wait_ld();
+            if (row >= rows) continue;
+            if (vec && col0 + c + 32 <= m) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    st_global_v4(dst + c + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                 __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+            } else {
+                for (int i = 0; i < 32; ++i)
+                    if (col0 + c + i < m) dst[c + i] = __uint_as_float(v[i]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, kSgN);
     }
 }
 
@@ -194,12 +316,29 @@ int grid_for(int64_t work, int threads) {
     return (int)(b < 148 * 32 ? (b > 0 ? b : 1) : 148 * 32);
 }
 
-// Per-plan synthesiser state: the fp32 lag-window rows and a cuBLAS handle.
+// Per-plan synthesiser state: the transposed lag-window operand Bs and its tensor map.
 struct SynthCache {
-    float* a32 = nullptr;  // [n_batch * L][M]
-    cublasHandle_t blas = nullptr;
+    __nv_bfloat16* bs = nullptr;  // [np][3 rp]
+    int rp = 0, np = 0;
+    CUtensorMap tm_b;
     std::mutex mu;
 };
+
+size_t sg_smem() { return 1024 + (size_t)kSgStages * kSgStageBytes + 256; }
+
+// Once per device: the GEMM's dynamic shared-memory opt-in (function attributes are per device).
+pnce_status_t synth_device_setup() {
+    static std::mutex mu;
+    static std::vector<int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return pnce_internal::set_error(PNCE_ERR_CUDA, "cudaGetDevice failed");
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return PNCE_OK;
+    cudaError_t e = cudaFuncSetAttribute(k_synth_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem());
+    if (e != cudaSuccess) return pnce_internal::set_error(PNCE_ERR_CUDA, std::string("synth attr: ") + cudaGetErrorString(e));
+    done.push_back(dev);
+    return PNCE_OK;
+}
 
 pnce_status_t synth_cache(const PlanView& v, cudaStream_t st, SynthCache*& out) {
     using pnce_internal::set_error;
@@ -209,22 +348,27 @@ pnce_status_t synth_cache(const PlanView& v, cudaStream_t st, SynthCache*& out) 
         out = static_cast<SynthCache*>(*v.synth_cache);
         return PNCE_OK;
     }
+    pnce_status_t s = synth_device_setup();
+    if (s != PNCE_OK) return s;
     auto* sc = new SynthCache();
-    const int rows = v.cfg.n_batch * v.cfg.l;
-    cudaError_t e = cudaMalloc(&sc->a32, sizeof(float) * rows * (size_t)v.cfg.m);
+    const int nbl = v.cfg.n_batch * v.cfg.l;
+    sc->rp = (nbl + kSgK - 1) / kSgK * kSgK;
+    sc->np = (v.cfg.m + kSgN - 1) / kSgN * kSgN;
+    const size_t n = (size_t)sc->np * 3 * sc->rp;
+    cudaError_t e = cudaMalloc(&sc->bs, sizeof(__nv_bfloat16) * n);
     if (e != cudaSuccess) {
         delete sc;
-        return set_error(PNCE_ERR_CUDA, std::string("synth rows: ") + cudaGetErrorString(e));
+        return set_error(PNCE_ERR_CUDA, std::string("synth operand: ") + cudaGetErrorString(e));
     }
-    k_build_a32<<<grid_for((int64_t)rows * v.cfg.m, 256), 256, 0, st>>>(v.chips, sc->a32, v.cfg.m, v.cfg.l, rows,
-                                                                        v.cfg.m / v.cfg.n_batch);
+    k_build_bsyn<<<grid_for((int64_t)n, 256), 256, 0, st>>>(v.chips, sc->bs, v.cfg.m, v.cfg.l, nbl, sc->rp, sc->np,
+                                                            v.cfg.m / v.cfg.n_batch);
     pnce_internal::count_launch();
-    if (cublasCreate(&sc->blas) != CUBLAS_STATUS_SUCCESS) {
-        cudaFree(sc->a32);
+    s = pnce_internal::encode_tmap_k16(&sc->tm_b, sc->bs, 3 * sc->rp, sc->np, kSgN, 1);
+    if (s != PNCE_OK) {
+        cudaFree(sc->bs);
         delete sc;
-        return set_error(PNCE_ERR_CUDA, "cublasCreate failed");
+        return s;
     }
-    cublasSetMathMode(sc->blas, CUBLAS_PEDANTIC_MATH);  // true fp32 (no TF32): the body feeds parity tests
     *v.synth_cache = sc;
     out = sc;
     return PNCE_OK;
@@ -235,8 +379,7 @@ pnce_status_t synth_cache(const PlanView& v, cudaStream_t st, SynthCache*& out) 
 namespace pnce_internal {
 void synth_cache_free(void* cache) {
     auto* sc = static_cast<SynthCache*>(cache);
-    if (sc->blas) cublasDestroy(sc->blas);
-    if (sc->a32) cudaFree(sc->a32);
+    if (sc->bs) cudaFree(sc->bs);
     delete sc;
 }
 }  // namespace pnce_internal
@@ -282,49 +425,50 @@ pnce_status_t pnce_simulate_frames(const pnce_plan_t* plan, const float* h, doub
     SynthCache* sc = nullptr;
     pnce_status_t s = synth_cache(v, st, sc);
     if (s != PNCE_OK) return s;
-    // frame chunks so the fp32 body (2 F n_r M floats) and H planes stay bounded (~512 MB)
-    const int64_t per_frame = 2LL * c.n_r * c.m + 2LL * c.n_r * c.n_t * c.l;
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_frames, (int64_t)(128ll << 20) / per_frame));
+    // frame chunks so the fp32 body (2 F n_r M floats) and the split H stay bounded (~512 MB)
+    const int64_t per_frame = 2LL * c.n_r * c.m * 4 + 2LL * c.n_r * 3 * sc->rp * 2;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_frames, (int64_t)(512ll << 20) / per_frame));
+    // the split H starts 256-byte aligned after the body (TMA global addresses: 16 B)
+    const size_t y_bytes = ((size_t)2 * chunk * c.n_r * c.m * 4 + 255) & ~(size_t)255;
     const int64_t n_fb = n_frames * v.n_batches;
     double* power = nullptr;
-    float* work = nullptr;
+    uint8_t* work = nullptr;
     cudaError_t e = cudaMallocAsync(&power, sizeof(double) * n_fb, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(power, 0, sizeof(double) * n_fb, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&work, sizeof(float) * per_frame * chunk, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&work, y_bytes + (size_t)2 * chunk * c.n_r * 3 * sc->rp * 2, st);
     if (e != cudaSuccess) {
         if (power) cudaFreeAsync(power, st);
         return set_error(PNCE_ERR_CUDA, std::string("synth scratch: ") + cudaGetErrorString(e));
     }
     std::lock_guard<std::mutex> lock(sc->mu);
-    cublasSetStream(sc->blas, st);
     const size_t smem = sizeof(float) * c.m;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_synth_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cublasStatus_t bs = CUBLAS_STATUS_SUCCESS;
-    for (int64_t f0 = 0; f0 < n_frames && bs == CUBLAS_STATUS_SUCCESS; f0 += chunk) {
+    pnce_status_t ms = PNCE_OK;
+    for (int64_t f0 = 0; f0 < n_frames && ms == PNCE_OK; f0 += chunk) {
         const int64_t fc = std::min(chunk, n_frames - f0);
-        const int64_t nh = fc * c.n_r * (int64_t)c.n_t * c.l;
-        float* hp = work;                    // [2][fc][n_r][n_t][L]
-        float* y = work + 2 * nh;            // [2][fc][n_r][M]
+        const int64_t fr = fc * c.n_r;
+        const int64_t rows = 2 * fr;                                   // (plane, f, r)
+        float* y = reinterpret_cast<float*>(work);                     // [2][fc][n_r][M]
+        __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(work + y_bytes);  // [rows][3 rp]
         const float2* hf = reinterpret_cast<const float2*>(h) + f0 * c.n_r * (int64_t)c.n_t * c.l;
-        k_h_planes<<<grid_for(nh, 256), 256, 0, st>>>(hf, hp, nh);
-        pnce_internal::count_launch();
-        const int rows = (int)(2 * fc * c.n_r);  // both planes: H row stride n_t*L is uniform
-        for (int b = 0; b < v.n_batches && bs == CUBLAS_STATUS_SUCCESS; ++b) {
+        CUtensorMap tm_h;
+        ms = pnce_internal::encode_tmap_k16(&tm_h, hs, 3 * sc->rp, rows, kSgM, 1);
+        for (int b = 0; b < v.n_batches && ms == PNCE_OK; ++b) {
             const int n_tx = std::min(c.n_batch, c.n_t - b * c.n_batch);
-            const float one = 1.f, zero = 0.f;
-            // column-major: Y^T [M x rows] = A^T [M x K] . H_b^T [K x rows]
-            bs = cublasSgemm(sc->blas, CUBLAS_OP_N, CUBLAS_OP_N, c.m, rows, n_tx * c.l, &one, sc->a32, c.m,
-                             hp + (int64_t)b * c.n_batch * c.l, c.n_t * c.l, &zero, y, c.m);
-            if (bs != CUBLAS_STATUS_SUCCESS) break;
-            k_synth_assemble<<<(unsigned)(fc * c.n_r), kSynThreads, smem, st>>>(
+            k_h_split<<<grid_for(rows * sc->rp, 256), 256, 0, st>>>(hf, hs, fr, c.n_t, c.l, b, c.n_batch, n_tx, sc->rp);
+            pnce_internal::count_launch();
+            const dim3 grid((unsigned)((rows + kSgM - 1) / kSgM), (unsigned)(sc->np / kSgN));
+            k_synth_gemm<<<grid, kSgThreads, sg_smem(), st>>>(tm_h, sc->tm_b, y, rows, c.m, 3 * sc->rp / kSgK);
+            pnce_internal::count_launch();
+            k_synth_assemble<<<(unsigned)fr, kSynThreads, smem, st>>>(
                 v.chips, hf, y, reinterpret_cast<float2*>(iq) + f0 * v.n_batches * c.n_r * (int64_t)S,
                 power + f0 * v.n_batches, b, c.m, c.c, c.l, c.n_t, c.n_r, c.n_batch, v.n_batches, spacing,
-                fc * c.n_r * (int64_t)c.m);
+                fr * (int64_t)c.m);
             pnce_internal::count_launch();
         }
     }
     e = cudaGetLastError();
-    if (e == cudaSuccess && bs == CUBLAS_STATUS_SUCCESS && std::isfinite(snr_db)) {
+    if (e == cudaSuccess && ms == PNCE_OK && std::isfinite(snr_db)) {
         const int64_t n_samples = n_fb * c.n_r * (int64_t)S;
         k_synth_noise<<<grid_for((n_samples + 1) / 2, 256), 256, 0, st>>>(
             reinterpret_cast<float2*>(iq), power, n_samples, (int64_t)c.n_r * S, c.n_r, c.m, c.l, c.n_t, c.n_batch,
@@ -334,7 +478,7 @@ pnce_status_t pnce_simulate_frames(const pnce_plan_t* plan, const float* h, doub
     }
     cudaFreeAsync(work, st);
     cudaFreeAsync(power, st);
-    if (bs != CUBLAS_STATUS_SUCCESS) return set_error(PNCE_ERR_CUDA, "cublasSgemm failed: " + std::to_string((int)bs));
+    if (ms != PNCE_OK) return ms;
     if (e != cudaSuccess) return set_error(PNCE_ERR_CUDA, std::string("k_synth: ") + cudaGetErrorString(e));
     return PNCE_OK;
 }

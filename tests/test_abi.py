@@ -64,3 +64,12 @@ def test_host_entry_points_without_gpu(built):
     with pytest.raises(P.ZeroStateError):
         _lib.check(built.pnce_config_check(ctypes.byref(zero)))
     assert built.pnce_kernel_launches() == 0
+
+
+def test_no_library_gemm(built):
+    """The synthesiser's body GEMM runs on the library's own tcgen05 kernel (k_synth_gemm):
+    no cuBLAS import or dependency is left in libpnce_b200.so."""
+    und = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in und.lower()
+    deps = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in deps.lower()
