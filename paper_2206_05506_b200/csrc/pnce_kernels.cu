@@ -64,7 +64,7 @@ std::atomic<int64_t> g_launches{0};
 struct Knobs {
     int epi8, group_fused, group_packed, group_packed_ldg, t16_g, narrow_g;
     int store_hint, raw_pol, split_drain, packed_mode, scored_g, narrow, mid, fused_mode, narrow_ldg;
-    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages;
+    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi;
 };
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -84,7 +84,7 @@ const Knobs& knobs() {
         r.raw_pol = env_int("PNCE_TUNE_RAW_POL", -1);
         r.split_drain = env_int("PNCE_TUNE_SPLIT_DRAIN", 1);
         r.packed_mode = env_int("PNCE_TUNE_PACKED_MODE", 0);
-        r.scored_g = env_int("PNCE_TUNE_SCORED_G", 256);
+        r.scored_g = env_int("PNCE_TUNE_SCORED_G", 512);
         r.narrow = env_int("PNCE_TUNE_NARROW", 1);
         r.mid = env_int("PNCE_TUNE_MID", 1);
         r.fused_mode = env_int("PNCE_TUNE_FUSED_MODE", -1);
@@ -92,9 +92,10 @@ const Knobs& knobs() {
         r.a_reuse = env_int("PNCE_TUNE_A_REUSE", 1);
         r.scr_pol = env_int("PNCE_TUNE_SCR_POL", 1);
         r.scr_slots = env_int("PNCE_TUNE_SCR_SLOTS", -1);
-        r.truth_slots = env_int("PNCE_TUNE_TRUTH_SLOTS", 3);
+        r.truth_slots = env_int("PNCE_TUNE_TRUTH_SLOTS", 2);
         r.ab_stages = env_int("PNCE_TUNE_AB_STAGES", -1);
         r.raw_stages = env_int("PNCE_TUNE_RAW_STAGES", -1);
+        r.scored_epi = env_int("PNCE_TUNE_SCORED_EPI", 8);
         return r;
     }();
     return k;
@@ -794,10 +795,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     constexpr bool RAW = MODE == kModeFusedTma;     // f32 rows TMA-staged, converted
     constexpr bool FLDG = MODE == kModeFusedLdg;    // f32 rows LDG'd, converted
     constexpr bool PLDG = MODE == kModePackedLdg;   // packed 16-bit rows LDG'd
-    // Warp layout: the scored variant (truth / stats / per-link errors) trades converter
-    // warps for epilogue warps where the converter allows it: its drain does ~4x the work.
-    // (packed/TMA mode has no converter work: EPI8 moves 4 of those warps to the epilogue)
-    constexpr int kCW = ((SCORED || EPI8) && (RAW || A_TMA)) ? 4 : kConvWarps;
+    // Warp layout: EPI8 trades 4 converter warps for epilogue warps (the scored variant's
+    // default: its drain does ~4x the work; packed/TMA mode has no converter work)
+    constexpr int kCW = (EPI8 && (RAW || A_TMA)) ? 4 : kConvWarps;
     constexpr int kEW0 = kConvWarp0 + kCW;
     constexpr int kEW = kWarps - kEW0;
     // converter warps arriving per stage (both CTAs): all 8 (RAW), one 4-warp group (FLDG),
@@ -920,16 +920,24 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #endif
                     fence_proxy_async_global();
                 }
+#ifdef PNCE_DIAG_NO_B
+                // diagnostic: no circulant loads (B stage left as is; results are garbage)
+                if (leader) mbar_arrive_expect_tx(&full[stage], (A_TMA ? 2 * a_bytes : 0u) + (from_scr ? 2 * a_bytes : 0u));
+                (void)sb;
+#else
                 if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes + (from_scr ? 2 * a_bytes : 0u));
+#endif
                 if (A_TMA)
                     tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
                 if (from_scr)  // keep the stage in L2 for the row tile's later groups
                     tma_load_2d_pair(sa, &tm_scr, fb_leader, 0, scr_row(r, kb),
                                      g == p.n_groups - 1 ? policy_evict_first()
                                                          : (p.scr_pol ? policy_evict_last() : policy_evict_normal()));
+#ifndef PNCE_DIAG_NO_B
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
                                      g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
+#endif
                 if (++stage == S) { stage = 0; phase ^= 1u; }
                 if (++kb == p.k_blocks) {
                     kb = 0;
@@ -1142,23 +1150,31 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         const bool ok0 = k < p.m, ok1 = k + 1 < p.m;
                         const int col_byte = h * 64 + (lane & 15) * 4;
 #ifndef PNCE_DIAG_NO_CONV
+                        // all of the chunk's LDS first, then the conversions and STS: the loads
+                        // overlap instead of one LDS -> F2FP -> STS round trip per link pair
+                        constexpr int kIt = kLinksPerTile / (2 * kCW);
+                        float4 v[kIt];
 #pragma unroll
-                        for (int it = 0; it < kLinksPerTile / (2 * kCW); ++it) {
+                        for (int it = 0; it < kIt; ++it) {
                             const int idx = cw + kCW * it;  // 0..31
                             const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
                             const uint32_t src = raw + link * (p.raw_row_floats * 4);
-                            float4 v;
                             if (slack == 0) {
-                                v = ld_shared_v4f(src);
+                                v[it] = ld_shared_v4f(src);
                             } else {
                                 const float2 a = ld_shared_v2f(src);
                                 const float2 b = ld_shared_v2f(src + 8);
-                                v = make_float4(a.x, a.y, b.x, b.y);
+                                v[it] = make_float4(a.x, a.y, b.x, b.y);
                             }
-                            if (!ok0) { v.x = 0.f; v.y = 0.f; }
-                            if (!ok1) { v.z = 0.f; v.w = 0.f; }
-                            st_shared_u32(swz(sa, (int)a_row(link, 0), col_byte), pack2(v.x, v.z, p.bf16));
-                            st_shared_u32(swz(sa, (int)a_row(link, 1), col_byte), pack2(v.y, v.w, p.bf16));
+                        }
+#pragma unroll
+                        for (int it = 0; it < kIt; ++it) {
+                            const int idx = cw + kCW * it;
+                            const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
+                            if (!ok0) { v[it].x = 0.f; v[it].y = 0.f; }
+                            if (!ok1) { v[it].z = 0.f; v[it].w = 0.f; }
+                            st_shared_u32(swz(sa, (int)a_row(link, 0), col_byte), pack2(v[it].x, v[it].z, p.bf16));
+                            st_shared_u32(swz(sa, (int)a_row(link, 1), col_byte), pack2(v[it].y, v[it].w, p.bf16));
                         }
 #else
                         (void)raw; (void)ok0; (void)ok1; (void)col_byte;
@@ -1905,6 +1921,9 @@ static cudaError_t set_smem_attrs() {
     if (e == cudaSuccess && (MODE == kModeFusedTma || MODE == kModePacked))
         e = cudaFuncSetAttribute(k_correlate<MODE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemLimit);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_correlate<MODE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemLimit);
     if (e == cudaSuccess && MODE == kModeFusedTma)
         e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -1921,8 +1940,10 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
     // -5 % for the fused path (converters become the bottleneck); PNCE_TUNE_EPI8 overrides
     const int epi8_env = knobs().epi8;
     const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
-    if (scored)
-        k_correlate<MODE, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
+    if (scored && knobs().scored_epi == 4)
+        k_correlate<MODE, true, false><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
+    else if (scored)
+        k_correlate<MODE, true, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else if ((MODE == kModeFusedTma || MODE == kModePacked) && epi8)
         k_correlate<MODE, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else
@@ -2532,12 +2553,13 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.bar_bytes = 2048;
             budget -= 1024;
         }
-        // scored drain: truth staged through a per-thread LDGSTS ring (8 epilogue warps x
+        // scored drain: truth staged through a per-thread LDGSTS ring (epilogue warps x
         // slots x 2 KB) when the truth runs are 16-byte aligned (PNCE_TUNE_TRUTH_SLOTS, 0 = off)
+        const int epi_warps = kn.scored_epi == 4 ? 4 : 8;
         if (scored && truth && (p->cfg.l % 2) == 0 && (reinterpret_cast<uintptr_t>(truth) & 15) == 0 &&
             (prm.g_cols & 31) == 0 && kn.truth_slots >= 2 && kn.truth_slots <= 4) {
             prm.truth_slots = kn.truth_slots;
-            budget -= (int64_t)8 * prm.truth_slots * 2048;
+            budget -= (int64_t)epi_warps * prm.truth_slots * 2048;
         }
         int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
         if (kn.ab_stages > 0) ab = std::min<int>((int)(budget / prm.stage_bytes), kn.ab_stages);
@@ -2551,7 +2573,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         if (prm.a_reuse && prm.k_blocks < prm.stages) prm.scr_slots = 2;
         prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + prm.bar_bytes +
                                    (size_t)prm.raw_stages * prm.raw_stage_bytes);
-        const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)8 * prm.truth_slots * 2048;
+        const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)epi_warps * prm.truth_slots * 2048;
         const int grid = pair_grid(p, prm);
         if (prm.a_reuse) {
             // [slots][clusters][2 CTAs][k_blocks] A stages of 128 rows x 128 B, owned by the

@@ -61,10 +61,12 @@ def default_run(tmp_path_factory):
     return _run(tmp_path_factory.mktemp("knobs"), "default", {})
 
 
-@pytest.mark.parametrize("knob", ["PNCE_TUNE_SPLIT_DRAIN", "PNCE_TUNE_A_REUSE", "PNCE_TUNE_TRUTH_SLOTS",
-                                  "PNCE_TUNE_NARROW", "PNCE_TUNE_NARROW_LDG", "PNCE_TUNE_MID"])
-def test_variant_bit_identical(default_run, tmp_path, knob):
-    other = _run(tmp_path, knob, {knob: "0"})
+@pytest.mark.parametrize("knob,value", [("PNCE_TUNE_SPLIT_DRAIN", "0"), ("PNCE_TUNE_A_REUSE", "0"),
+                                        ("PNCE_TUNE_TRUTH_SLOTS", "0"), ("PNCE_TUNE_TRUTH_SLOTS", "3"),
+                                        ("PNCE_TUNE_NARROW", "0"), ("PNCE_TUNE_NARROW_LDG", "0"), ("PNCE_TUNE_MID", "0"),
+                                        ("PNCE_TUNE_SCORED_G", "256"), ("PNCE_TUNE_SCORED_EPI", "4")])
+def test_variant_bit_identical(default_run, tmp_path, knob, value):
+    other = _run(tmp_path, knob + value, {knob: value})
     for key in default_run.files:
         a, b = default_run[key], other[key]
         if key.endswith("_stats") or key.endswith("_link"):

@@ -22,7 +22,8 @@ t = d.get("tensor16_leg") or {}
 c4 = d.get("cfg4_leg") or {}
 print(f"{name:24s} fused {d['us_per_frame']:.4f} us ({d['roofline']['frac']:.3f})  gemm {g.get('us_per_frame', 0):.4f} ({g.get('frac_of_bf16_peak', 0):.3f})"
       f"  scored {q.get('scored_us_per_frame', 0):.3f}  t16 {t.get('us_per_frame', 0):.3f}"
-      + (f"  c4f {c4['fused']['us_per_frame']:.2f} c4g {c4['gemm']['us_per_frame']:.2f}" if c4 else ""), flush=True)
+      + (f"  c4f {c4['fused']['us_per_frame']:.2f} c4g {c4['gemm']['us_per_frame']:.2f}" if c4 else "")
+      + f"  [{(d.get('clocks') or {}).get('sm_mhz')} MHz {(d.get('clocks') or {}).get('power_w')} W]", flush=True)
 PY
   done
 done < "$SPEC"
