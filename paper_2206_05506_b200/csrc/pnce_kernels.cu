@@ -64,7 +64,7 @@ std::atomic<int64_t> g_launches{0};
 struct Knobs {
     int epi8, group_fused, group_packed, group_packed_ldg, t16_g, narrow_g;
     int store_hint, raw_pol, split_drain, packed_mode, scored_g, narrow, mid, fused_mode, narrow_ldg;
-    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi;
+    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi, t16_epi;
 };
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -96,6 +96,7 @@ const Knobs& knobs() {
         r.ab_stages = env_int("PNCE_TUNE_AB_STAGES", -1);
         r.raw_stages = env_int("PNCE_TUNE_RAW_STAGES", -1);
         r.scored_epi = env_int("PNCE_TUNE_SCORED_EPI", 8);
+        r.t16_epi = env_int("PNCE_TUNE_T16_EPI", 8);
         return r;
     }();
     return k;
@@ -787,6 +788,32 @@ __device__ __forceinline__ void t16_fold(const CorrParams& p, uint32_t t_part, u
     if (!last) tmem_wait_st();
 }
 
+// Intermediate tensor16 fold (every accumulation unit but the last): elementwise on the
+// warp's 32 TMEM lanes, layout-agnostic, so the 32x32b.x32 shape (32 columns per thread per
+// load) halves the instruction count of the 16x256b path; the next 32 columns are in flight
+// while this block is folded.  total = fl32(total + fl32(fl32(partial) * fl32(1/M))), two
+// roundings as halprec.py:104-117; a non-finite partial or total leaves `nf` non-finite.
+__device__ __forceinline__ void t16_fold_mid(const CorrParams& p, uint32_t t_part, uint32_t t_tot, bool first,
+                                             float& nf, int c0, int c1) {
+    uint32_t pa[32], ta[32];
+    for (int c = c0; c < c1; c += 32) {
+        tmem_ld32_nowait(t_part + c, pa);
+        if (!first) tmem_ld32_nowait(t_tot + c, ta);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float x = p.acc16 ? __half2float(__ushort_as_half((unsigned short)(pa[i] & 0xffffu)))
+                                    : __uint_as_float(pa[i]);
+            const float y = __fmul_rn(x, p.inv_m);
+            const float t = first ? y : __fadd_rn(__uint_as_float(ta[i]), y);
+            nf = fmaf(t, 0.f, nf);   // inf / NaN anywhere -> NaN (sticky)
+            ta[i] = __float_as_uint(t);
+        }
+        tmem_st32(t_tot + c, ta);
+    }
+    tmem_wait_st();
+}
+
 template <int MODE, bool SCORED, bool EPI8 = false, bool T16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
@@ -1396,22 +1423,40 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + quarter * 16 + (lane >> 2);
                 const int n0 = g * p.g_cols + colp;
                 bool sat[2] = {false, false};
+                float nf_mid = 0.f;
                 for (int u = 0; u < n_units; ++u) {
                     mbar_wait(&tfull[acc], acc_phase);
                     tc_fence_after();
+                    if (u < n_units - 1) {
+                        // intermediate unit: elementwise over the warp's 32 lanes (both 16-lane
+                        // blocks); with 8 epilogue warps the two warps of a quarter split the columns
+                        const uint32_t lanes = (uint32_t)(quarter * 32) << 16;
+                        const int half_cols = (p.g_cols / 64) * 32;   // a multiple of 32
+                        const int c0 = kBlocksPerWarp == 2 ? 0 : bb0 * half_cols;
+                        const int c1 = kBlocksPerWarp == 2 ? p.g_cols : (bb0 ? p.g_cols : half_cols);
+                        t16_fold_mid(p, tmem_base + lanes + (uint32_t)(acc * p.g_cols),
+                                     tmem_base + lanes + (uint32_t)(p.acc_stages * p.g_cols), u == 0, nf_mid, c0, c1);
+                    } else {
 #pragma unroll
-                    for (int k = 0; k < kBlocksPerWarp; ++k) {
-                        const int bb = bb0 + k;
-                        const EpiLink e = make_link(p, link0 + 8 * bb);
-                        const uint32_t lanes = (uint32_t)(quarter * 32 + 16 * bb) << 16;
-                        t16_fold(p, tmem_base + lanes + (uint32_t)(acc * p.g_cols),
-                                 tmem_base + lanes + (uint32_t)(p.acc_stages * p.g_cols), e, n0, u == 0,
-                                 u == n_units - 1, sat[k]);
+                        for (int k = 0; k < kBlocksPerWarp; ++k) {
+                            const int bb = bb0 + k;
+                            const EpiLink e = make_link(p, link0 + 8 * bb);
+                            const uint32_t lanes = (uint32_t)(quarter * 32 + 16 * bb) << 16;
+                            t16_fold(p, tmem_base + lanes + (uint32_t)(acc * p.g_cols),
+                                     tmem_base + lanes + (uint32_t)(p.acc_stages * p.g_cols), e, n0, u == 0,
+                                     u == n_units - 1, sat[k]);
+                        }
                     }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + (uint32_t)(acc * 8));
                     if (++acc == p.acc_stages) { acc = 0; acc_phase ^= 1; }
+                }
+                if (nf_mid != 0.f) {
+                    // thread = TMEM lane = A row 32q + lane of this CTA: link (r / 16) * 8 + r % 8
+                    const int r = quarter * 32 + lane;
+                    const int64_t link = ((int64_t)mt * 2 + rank) * kLinksPerTile + ((r >> 4) << 3) + (r & 7);
+                    if (link < p.total_links) atomicOr(p.sat_flags + (uint32_t)link / (uint32_t)p.n_r, 1u);
                 }
 #pragma unroll
                 for (int k = 0; k < kBlocksPerWarp; ++k) {
@@ -1926,6 +1971,9 @@ static cudaError_t set_smem_attrs() {
                                  kSmemLimit);
     if (e == cudaSuccess && MODE == kModeFusedTma)
         e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e == cudaSuccess && MODE == kModeFusedTma)
+        e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, true, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     return e;
 }
@@ -2599,8 +2647,12 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.acc16 = t16->acc16;
             prm.sat_flags = res->flags;
             if (t16->acc16) prm.idesc &= ~(3u << 4);  // c_format = F16: binary16 partials in TMEM
-            k_correlate<kModeFusedTma, false, false, true><<<grid, kThreadsK3, smem, st>>>(
-                res->tm_in, p->t16.tm_circ, prm.a_reuse ? res->tm_scr : p->t16.tm_circ, prm);
+            if (kn.t16_epi == 8)
+                k_correlate<kModeFusedTma, false, true, true><<<grid, kThreadsK3, smem, st>>>(
+                    res->tm_in, p->t16.tm_circ, prm.a_reuse ? res->tm_scr : p->t16.tm_circ, prm);
+            else
+                k_correlate<kModeFusedTma, false, false, true><<<grid, kThreadsK3, smem, st>>>(
+                    res->tm_in, p->t16.tm_circ, prm.a_reuse ? res->tm_scr : p->t16.tm_circ, prm);
             g_launches++;
             const pnce_cfg_t& c = p->cfg;
             k_t16_finish<<<(unsigned)n_fb, 256, 0, st>>>(taps, truth, stats, res->flags, c.n_r, c.n_t, c.n_batch,

@@ -64,7 +64,8 @@ def default_run(tmp_path_factory):
 @pytest.mark.parametrize("knob,value", [("PNCE_TUNE_SPLIT_DRAIN", "0"), ("PNCE_TUNE_A_REUSE", "0"),
                                         ("PNCE_TUNE_TRUTH_SLOTS", "0"), ("PNCE_TUNE_TRUTH_SLOTS", "3"),
                                         ("PNCE_TUNE_NARROW", "0"), ("PNCE_TUNE_NARROW_LDG", "0"), ("PNCE_TUNE_MID", "0"),
-                                        ("PNCE_TUNE_SCORED_G", "256"), ("PNCE_TUNE_SCORED_EPI", "4")])
+                                        ("PNCE_TUNE_SCORED_G", "256"), ("PNCE_TUNE_SCORED_EPI", "4"),
+                                        ("PNCE_TUNE_T16_EPI", "4")])
 def test_variant_bit_identical(default_run, tmp_path, knob, value):
     other = _run(tmp_path, knob + value, {knob: value})
     for key in default_run.files:
