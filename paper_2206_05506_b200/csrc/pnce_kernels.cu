@@ -64,7 +64,7 @@ std::atomic<int64_t> g_launches{0};
 struct Knobs {
     int epi8, group_fused, group_packed, group_packed_ldg, t16_g, narrow_g;
     int store_hint, raw_pol, split_drain, packed_mode, scored_g, narrow, mid, fused_mode, narrow_ldg;
-    int a_reuse, scr_pol, scr_slots, truth_slots, a_stages, b_stages, raw_stages, scored_epi, t16_epi;
+    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi, t16_epi;
 };
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -93,8 +93,7 @@ const Knobs& knobs() {
         r.scr_pol = env_int("PNCE_TUNE_SCR_POL", 1);
         r.scr_slots = env_int("PNCE_TUNE_SCR_SLOTS", -1);
         r.truth_slots = env_int("PNCE_TUNE_TRUTH_SLOTS", 2);
-        r.a_stages = env_int("PNCE_TUNE_A_STAGES", -1);
-        r.b_stages = env_int("PNCE_TUNE_B_STAGES", -1);
+        r.ab_stages = env_int("PNCE_TUNE_AB_STAGES", -1);
         r.raw_stages = env_int("PNCE_TUNE_RAW_STAGES", -1);
         r.scored_epi = env_int("PNCE_TUNE_SCORED_EPI", 8);
         r.t16_epi = env_int("PNCE_TUNE_T16_EPI", 8);
@@ -305,6 +304,7 @@ struct CorrParams {
     int32_t nm;
     int32_t acc_stages;   // TMEM accumulator buffers (2 if 2*g_cols <= 512)
     int32_t k_blocks;
+    int32_t stages;
     int32_t raw_stages;      // FusedTma: f32 staging ring depth (half-K-block chunks)
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
@@ -319,9 +319,8 @@ struct CorrParams {
     int32_t split_drain;  // release the first N half of a single accumulator early (see k_correlate)
     int32_t truth_slots;  // scored drain: per-thread LDGSTS ring depth for the truth (0: register path)
     uint32_t truth_off;   // byte offset of the truth ring in dynamic shared memory (after the raw ring)
-    int32_t a_stages;        // A ring depth (16 KB slots: 128 sample rows x 64 K)
-    int32_t b_stages;        // B ring depth
-    uint32_t b_stage_bytes;  // B slot: n_mma x (nm / 2) circulant rows x 64 K x 2 B (this CTA's half)
+    uint32_t stage_bytes;
+    uint32_t tx_bytes;    // transaction bytes per stage for BOTH CTAs of the pair
     uint32_t idesc;
     uint32_t tmem_cols;
     int32_t n_r, n_t, n_batches, n_batch, l;
@@ -834,25 +833,18 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    // [A ring: SA x 16 KB][B ring: SB x b_stage_bytes][1 KB barrier block (+1 KB a_reuse)]
-    // [raw f32 ring][truth ring].  A (sample rows) and B (circulant rows) have separate rings:
-    // A comes from HBM (deep ring hides its latency), B from L2 (a few slots suffice).
-    const int SA = p.a_stages, SB = p.b_stages;
-    uint8_t* const a_ring = smem;
-    uint8_t* const b_ring = smem + (size_t)SA * (kBM * kBK * 2);
-    uint8_t* const bar_base = b_ring + (size_t)SB * p.b_stage_bytes;
-    uint64_t* a_full = reinterpret_cast<uint64_t*>(bar_base);
-    uint64_t* a_empty = a_full + SA;
-    uint64_t* b_full = a_empty + SA;
-    uint64_t* b_empty = b_full + SB;
-    uint64_t* tfull = b_empty + SB;
+    // [A/B stages][1 KB barrier block][raw f32 stages]
+    const int S = p.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint64_t* raw_full = tempty + 2;
     uint64_t* raw_empty = raw_full + (RAW ? p.raw_stages : 0);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + (RAW ? p.raw_stages : 0));
-    uint8_t* raw_base = bar_base + p.bar_bytes;
+    uint8_t* raw_base = smem + (size_t)S * p.stage_bytes + p.bar_bytes;
     // a_reuse: per (slot, K-block) "A stage stored" barriers in the second KB of the block
-    uint64_t* scr_full = reinterpret_cast<uint64_t*>(bar_base + 1024);
+    uint64_t* scr_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes + 1024);
     const bool reuse = RAW && p.a_reuse;
 
     const int warp = threadIdx.x >> 5;
@@ -861,17 +853,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const bool leader = rank == 0;
 
     if (threadIdx.x == 0) {
-        // Leader barriers collect both CTAs (the peer's TMA bytes and converter arrives land on
-        // the leader's full barriers): A full = the packed-A producer's expect_tx, or the
-        // converter warps of both CTAs (LDG modes: the one group that converts the job);
-        // B full = the circulant producer's expect_tx.  Empties: one multicast MMA commit.
-        for (int s = 0; s < SA; ++s) {
-            mbar_init(&a_full[s], A_TMA ? 1 : kConvArrivals);
-            mbar_init(&a_empty[s], 1);
-        }
-        for (int s = 0; s < SB; ++s) {
-            mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], 1);
+        for (int s = 0; s < S; ++s) {
+            // Leader: producer expect_tx + the converter warps of BOTH CTAs (the peer's TMA
+            // bytes and converter arrives land on the leader's barrier).
+            // (LDG mode: only one 4-warp group converts a given stage)
+            mbar_init(&full[s], 1 + kConvArrivals);
+            mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -927,62 +914,80 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const bool split = !T16 && p.split_drain && p.acc_stages == 1 && p.n_mma == 2;
 
 
-    // job j (one K-block of one tile) uses A slot j % SA and B slot j % SB
-    struct Ring {
-        int slot;
-        uint32_t phase;
-        int n;
-        __device__ __forceinline__ void next() {
-            if (++slot == n) { slot = 0; phase ^= 1u; }
-        }
-    };
-    auto a_addr = [&](int slot) { return smem_u32(a_ring + (size_t)slot * a_bytes); };
-    auto b_addr = [&](int slot) { return smem_u32(b_ring + (size_t)slot * p.b_stage_bytes); };
-
     if (warp == 0) {
         if (lane == 0) {
-            // ===== TMA producer: circulant rows into the B ring; bytes land on the leader
+            // ===== TMA producer: circulant rows (+ packed sample rows); bytes land on the leader
+            const uint64_t pol_in = p.raw_pol == 0 ? policy_evict_first()
+                                                   : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
             const uint64_t pol_circ = policy_evict_last();
-            int kb = 0, ti = 0, g = coords(0).y;
-            Ring rb{0, 0u, SB};
+            int kb = 0, ti = 0, stage = 0, mt = 0, g = 0;
+            { const int2 _c = coords(0); mt = _c.x; g = _c.y; }
+            uint32_t phase = 0;
+#ifdef PNCE_DIAG_PROF
+            uint64_t prof_scr_wait = 0;
+#endif
             PROF_BEGIN(2);
             for (int j = 0; j < jobs; ++j) {
-                mbar_wait(&b_empty[rb.slot], rb.phase ^ 1u);
+                mbar_wait(&empty[stage], phase ^ 1u);
                 PROF_MARK(0);
                 TRACE(0, j);
-                uint8_t* sb = b_ring + (size_t)rb.slot * p.b_stage_bytes;
-                const uint32_t fb_leader = mapa_shared(smem_u32(&b_full[rb.slot]), 0);
+                uint8_t* sa = smem + (size_t)stage * p.stage_bytes;
+                uint8_t* sb = sa + a_bytes;
+                const uint32_t fb_leader = mapa_shared(smem_u32(&full[stage]), 0);
+                const bool from_scr = reuse && g > 0;
+                const int r = ti / p.n_groups;
+                if (from_scr) {
+                    // group 0 of this row tile stored the converted A stage of K-block kb
+#ifdef PNCE_DIAG_PROF
+                    const uint64_t w0 = clock64();
+#endif
+                    mbar_wait(&scr_full[(r % p.scr_slots) * p.k_blocks + kb], (uint32_t)(r / p.scr_slots) & 1u);
+#ifdef PNCE_DIAG_PROF
+                    prof_scr_wait += clock64() - w0;
+#endif
+                    fence_proxy_async_global();
+                }
 #ifdef PNCE_DIAG_NO_B
-                // diagnostic: no circulant loads (B slot left as is; results are garbage)
-                if (leader) mbar_arrive(&b_full[rb.slot]);
-                (void)sb; (void)fb_leader; (void)pol_circ; (void)g;
+                // diagnostic: no circulant loads (B stage left as is; results are garbage)
+                if (leader) mbar_arrive_expect_tx(&full[stage], (A_TMA ? 2 * a_bytes : 0u) + (from_scr ? 2 * a_bytes : 0u));
+                (void)sb;
 #else
-                if (leader) mbar_arrive_expect_tx(&b_full[rb.slot], 2u * (uint32_t)p.n_mma * b_half_bytes);
+                if (leader) mbar_arrive_expect_tx(&full[stage], p.tx_bytes + (from_scr ? 2 * a_bytes : 0u));
+#endif
+                if (A_TMA)
+                    tma_load_2d_pair(sa, &tm_in, fb_leader, kb * kBK, mt * 2 * kBM + (int)rank * kBM, pol_in);
+                if (from_scr)  // keep the stage in L2 for the row tile's later groups
+                    tma_load_2d_pair(sa, &tm_scr, fb_leader, 0, scr_row(r, kb),
+                                     g == p.n_groups - 1 ? policy_evict_first()
+                                                         : (p.scr_pol ? policy_evict_last() : policy_evict_normal()));
+#ifndef PNCE_DIAG_NO_B
                 for (int jj = 0; jj < p.n_mma; ++jj)
                     tma_load_2d_pair(sb + jj * b_half_bytes, &tm_circ, fb_leader, kb * kBK,
                                      g * p.g_cols + jj * p.nm + (int)rank * (p.nm / 2), pol_circ);
 #endif
-                rb.next();
+                if (++stage == S) { stage = 0; phase ^= 1u; }
                 if (++kb == p.k_blocks) {
                     kb = 0;
-                    g = coords(++ti).y;
+                    { const int2 _c = coords(++ti); mt = _c.x; g = _c.y; }
                 }
                 PROF_MARK(1);
             }
             PROF_END(0, 2);
+#ifdef PNCE_DIAG_PROF
+            g_prof[blockIdx.x * kProfSlots + 15] = prof_scr_wait;
+#endif
         }
     } else if (warp == 1) {
         if (leader && lane == 0 && split) {
             // ===== MMA issuer, split-drain variant: per K-block the first-half MMAs (columns
             // [0, nm)) go as soon as the epilogue released that half; second-half MMAs of the
-            // jobs held meanwhile are issued once the whole accumulator is drained.
-            Ring ra{0, 0u, SA}, rb{0, 0u, SB};
-            uint32_t tphase = 0;
-            const int max_held = SA < SB ? SA : SB;
-            int pend_a0 = 0, pend_b0 = 0, pend_kb0 = 0;  // held jobs are consecutive (ring order, kb order)
-            auto issue_half = [&](int sa_slot, int sb_slot, int kb, int jj) {
-                const uint32_t sa = a_addr(sa_slot);
-                const uint32_t sb = b_addr(sb_slot);
+            // stages held meanwhile are issued once the whole accumulator is drained.
+            int stage = 0;
+            uint32_t phase = 0, tphase = 0;
+            int pend_stage0 = 0, pend_kb0 = 0;  // held stages are consecutive (ring order, kb order)
+            auto issue_half = [&](int st, int kb, int jj) {
+                const uint32_t sa = smem_u32(smem + (size_t)st * p.stage_bytes);
+                const uint32_t sb = sa + a_bytes;
 #pragma unroll
                 for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                     const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
@@ -1001,41 +1006,35 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 auto flush = [&]() {
                     tc_fence_after();
                     hi_ok = true;
-                    int sa_slot = pend_a0, sb_slot = pend_b0;
+                    int st = pend_stage0;
                     for (int i = 0; i < np; ++i) {
-                        issue_half(sa_slot, sb_slot, pend_kb0 + i, 1);
-                        umma_commit_pair(&a_empty[sa_slot]);
-                        umma_commit_pair(&b_empty[sb_slot]);
-                        if (++sa_slot == SA) sa_slot = 0;
-                        if (++sb_slot == SB) sb_slot = 0;
+                        issue_half(st, pend_kb0 + i, 1);
+                        umma_commit_pair(&empty[st]);
+                        if (++st == S) st = 0;
                     }
                     np = 0;
                 };
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
-                    if (!hi_ok && np == max_held) {  // every slot held: wait for the whole drain
+                    if (!hi_ok && np == S) {  // every stage held: wait for the whole drain
                         mbar_wait(&tempty[0], tphase ^ 1);
                         flush();
                     }
-                    mbar_wait(&a_full[ra.slot], ra.phase);
-                    mbar_wait(&b_full[rb.slot], rb.phase);
+                    mbar_wait(&full[stage], phase);
                     PROF_MARK(1);
                     TRACE(2, ti * p.k_blocks + kb);
                     tc_fence_after();
                     if (!hi_ok && mbar_test_wait(&tempty[0], tphase ^ 1)) flush();
-                    issue_half(ra.slot, rb.slot, kb, 0);
+                    issue_half(stage, kb, 0);
                     if (hi_ok) {
-                        issue_half(ra.slot, rb.slot, kb, 1);
-                        umma_commit_pair(&a_empty[ra.slot]);
-                        umma_commit_pair(&b_empty[rb.slot]);
+                        issue_half(stage, kb, 1);
+                        umma_commit_pair(&empty[stage]);
                     } else {
                         if (np++ == 0) {
-                            pend_a0 = ra.slot;
-                            pend_b0 = rb.slot;
+                            pend_stage0 = stage;
                             pend_kb0 = kb;
                         }
                     }
-                    ra.next();
-                    rb.next();
+                    if (++stage == S) { stage = 0; phase ^= 1u; }
                     PROF_MARK(2);
                 }
                 if (!hi_ok) {
@@ -1048,9 +1047,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             PROF_END(2, 3);
         } else if (leader && lane == 0) {
             // ===== MMA issuer (leader CTA, single thread) for the whole pair
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            Ring ra{0, 0u, SA}, rb{0, 0u, SB};
+            int acc = 0, stage = 0;
+            uint32_t acc_phase = 0, phase = 0;
 #ifdef PNCE_DIAG_PROF
             const uint64_t t_start = clock64();
 #endif
@@ -1068,14 +1066,15 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         d_tmem = tmem_base + (uint32_t)(acc * p.g_cols);
                     }
 #ifndef PNCE_DIAG_NO_FULLWAIT
-                    mbar_wait(&a_full[ra.slot], ra.phase);
-                    mbar_wait(&b_full[rb.slot], rb.phase);
+                    mbar_wait(&full[stage], phase);
+#else
+                    (void)phase;
 #endif
                     PROF_MARK(1);
                     TRACE(2, j);
                     tc_fence_after();
-                    const uint32_t sa = a_addr(ra.slot);
-                    const uint32_t sb = b_addr(rb.slot);
+                    const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                    const uint32_t sb = sa + a_bytes;
 #pragma unroll
                     for (int ks = 0; ks < kBK / kUmmaK; ++ks) {
                         const uint64_t ad = make_sdesc(sa + ks * 32, 16, 1024, 2);
@@ -1084,12 +1083,10 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             umma_f16_ss_pair(d_tmem + (uint32_t)(jj * p.nm), ad, bd, p.idesc, (kc | ks) != 0);
                         }
                     }
-                    umma_commit_pair(&a_empty[ra.slot]);
-                    umma_commit_pair(&b_empty[rb.slot]);
+                    umma_commit_pair(&empty[stage]);
                     TRACE(3, j);
                     (void)j;
-                    ra.next();
-                    rb.next();
+                    if (++stage == S) { stage = 0; phase ^= 1u; }
                     PROF_MARK(2);
                     if (++kc == p.chunk_kb || kb == p.k_blocks - 1) {
                         umma_commit_pair(&tfull[acc]);
@@ -1142,24 +1139,6 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
             }
             PROF_END(5, 2);
-        } else if (A_TMA && lane == 0) {
-            // ===== packed-operand producer: the 16-bit sample rows into the A ring
-            const uint64_t pol_in = p.raw_pol == 0 ? policy_evict_first()
-                                                   : (p.raw_pol == 2 ? policy_evict_last() : policy_evict_normal());
-            int kb = 0, ti = 0, mt = coords(0).x;
-            Ring ra{0, 0u, SA};
-            for (int j = 0; j < jobs; ++j) {
-                mbar_wait(&a_empty[ra.slot], ra.phase ^ 1u);
-                const uint32_t fa_leader = mapa_shared(smem_u32(&a_full[ra.slot]), 0);
-                if (leader) mbar_arrive_expect_tx(&a_full[ra.slot], 2u * a_bytes);
-                tma_load_2d_pair(a_ring + (size_t)ra.slot * a_bytes, &tm_in, fa_leader, kb * kBK,
-                                 mt * 2 * kBM + (int)rank * kBM, pol_in);
-                ra.next();
-                if (++kb == p.k_blocks) {
-                    kb = 0;
-                    mt = coords(++ti).x;
-                }
-            }
         }
     } else if (warp >= kConvWarp0 && warp < kEW0) {
         if (RAW) {
@@ -1172,42 +1151,18 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #endif
             PROF_BEGIN(3);
             for (int j = 0; j < jobs; ++j) {
-                const uint32_t sa = a_addr(stage);
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
                 if (reuse && g > 0) {
-                    // the A stage comes from the scratch by TMA (group 0 of this row tile stored
-                    // it): converter warp 0 issues the load -- the leader's with the expect_tx of
-                    // both CTAs' bytes -- the other converter warps only keep the arrival count
-                    mbar_wait(&a_empty[stage], phase ^ 1u);
-                    const uint32_t fa_leader = mapa_shared(smem_u32(&a_full[stage]), 0);
-                    if (cw == 0) {
-                      if (lane == 0) {
-                        const int r = ti / p.n_groups;
-#ifdef PNCE_DIAG_PROF
-                        const uint64_t w0 = clock64();
-#endif
-                        mbar_wait(&scr_full[(r % p.scr_slots) * p.k_blocks + kb], (uint32_t)(r / p.scr_slots) & 1u);
-#ifdef PNCE_DIAG_PROF
-                        g_prof[blockIdx.x * kProfSlots + 15] += clock64() - w0;
-#endif
-                        fence_proxy_async_global();
-                        if (leader) mbar_arrive_expect_tx(&a_full[stage], 2u * a_bytes);
-                        // keep the stage in L2 for the row tile's later groups
-                        tma_load_2d_pair(a_ring + (size_t)stage * a_bytes, &tm_scr, fa_leader, 0, scr_row(r, kb),
-                                         g == p.n_groups - 1 ? policy_evict_first()
-                                                             : (p.scr_pol ? policy_evict_last() : policy_evict_normal()));
-                        if (!leader) mbar_arrive_remote(fa_leader);
-                      }
-                      __syncwarp();
-                    } else {
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_remote(fa_leader);
-                    }
+                    // the A stage comes from the scratch by TMA: only keep the arrival count
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                 } else {
                     // staged f32 chunks -> A stage.  Per chunk a warp converts 8 links: lanes
                     // 0-15 link a, lanes 16-31 link a+4 (so the two Re rows fall in different
                     // swizzle halves: conflict-free STS); lane l handles samples 2(l%16), +1
                     // (one LDS.128 of the link's 256 B row, two STS.32 into its Re / Im rows).
-                    mbar_wait(&a_empty[stage], phase ^ 1u);
+                    mbar_wait(&empty[stage], phase ^ 1u);
                     PROF_MARK(0);
                     if (cw == 0 && lane == 0) TRACE(8, j);
 #pragma unroll
@@ -1262,7 +1217,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     if (lane == 0) {
                         // proxy fence above completed this warp's STS; plain (CTA-scope
                         // release) arrive on the leader's barrier, no GPU-scope membar
-                        mbar_arrive_remote(mapa_shared(smem_u32(&a_full[stage]), 0));
+                        mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                         if (cw == 0) TRACE(9, j);
                     }
                     if (reuse) {
@@ -1312,7 +1267,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                     }
                 }
                 PROF_MARK(2);
-                if (++stage == SA) { stage = 0; phase ^= 1u; }
+                if (++stage == S) { stage = 0; phase ^= 1u; }
                 if (++kb == p.k_blocks) {
                     kb = 0;
                     { const int2 _c = coords(++ti); mt = _c.x; g = _c.y; }
@@ -1338,8 +1293,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const bool vec = ((p.samples | p.c) & 1) == 0 && (reinterpret_cast<uintptr_t>(p.iq) & 15) == 0;
             float4 v[kLinksPerTile / 4];
             int kb = gsel % p.k_blocks, ti = gsel / p.k_blocks;
-            int stage = gsel % SA;
-            uint32_t phase = (uint32_t)(gsel / SA) & 1u;
+            int stage = gsel % S;
+            uint32_t phase = (uint32_t)(gsel / S) & 1u;
             auto load_job = [&](int lti, int lkb) {
                 const int mt = (cid + lti * n_clusters) / p.n_groups;
                 const int64_t link0 = ((int64_t)mt * 2 + rank) * kLinksPerTile + gw;
@@ -1364,8 +1319,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (gsel < jobs) load_job(ti, kb);
             PROF_BEGIN(3);
             for (int j = gsel; j < jobs; j += 2) {
-                const uint32_t sa = a_addr(stage);
-                mbar_wait(&a_empty[stage], phase ^ 1u);
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                mbar_wait(&empty[stage], phase ^ 1u);
                 PROF_MARK(0);
                 if (cw == 0 && lane == 0) TRACE(8, j);
 #pragma unroll
@@ -1378,12 +1333,12 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_remote(mapa_shared(smem_u32(&a_full[stage]), 0));
+                    mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                     if (cw == 0) TRACE(9, j);
                 }
                 // advance two jobs and prefetch the next one (after the fence)
                 stage += 2;
-                while (stage >= SA) { stage -= SA; phase ^= 1u; }
+                while (stage >= S) { stage -= S; phase ^= 1u; }
                 kb += 2;
                 while (kb >= p.k_blocks) { kb -= p.k_blocks; ++ti; }
                 if (j + 2 < jobs) load_job(ti, kb);
@@ -1402,8 +1357,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             const int tid = (cw & 1) * 32 + lane;  // 0..63
             uint4 v[16];
             int kb = gsel % p.k_blocks, ti = gsel / p.k_blocks;
-            int stage = gsel % SA;
-            uint32_t phase = (uint32_t)(gsel / SA) & 1u;
+            int stage = gsel % S;
+            uint32_t phase = (uint32_t)(gsel / S) & 1u;
             auto load_job = [&](int lti, int lkb) {
                 const int mt = (cid + lti * n_clusters) / p.n_groups;
                 const int64_t row0 = ((int64_t)mt * 2 + rank) * kBM;
@@ -1424,8 +1379,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
             if (gsel < jobs) load_job(ti, kb);
             PROF_BEGIN(3);
             for (int j = gsel; j < jobs; j += kGroups) {
-                const uint32_t sa = a_addr(stage);
-                mbar_wait(&a_empty[stage], phase ^ 1u);
+                const uint32_t sa = smem_u32(smem + (size_t)stage * p.stage_bytes);
+                mbar_wait(&empty[stage], phase ^ 1u);
                 PROF_MARK(0);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
@@ -1434,9 +1389,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&a_full[stage]), 0));
+                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&full[stage]), 0));
                 stage += kGroups;
-                while (stage >= SA) { stage -= SA; phase ^= 1u; }
+                while (stage >= S) { stage -= S; phase ^= 1u; }
                 kb += kGroups;
                 while (kb >= p.k_blocks) { kb -= p.k_blocks; ++ti; }
                 if (j + kGroups < jobs) load_job(ti, kb);
@@ -1863,7 +1818,8 @@ struct Tiling {
     int n_mma;       // pair MMAs per k-step (N = nm each)
     int nm;
     int acc_stages;  // TMEM accumulator buffers
-    uint32_t b_stage_bytes;  // B ring slot: (g_cols / 2) circulant rows x 64 K x 2 B per CTA
+    int stages;      // smem pipeline depth
+    uint32_t stage_bytes;
     uint32_t tmem_cols;
     CUtensorMap tm_circ;  // circulant rows, box = nm/2 rows x 64 K
 };
@@ -1994,7 +1950,9 @@ static void make_tiling(Tiling& t, int r_total, int max_group, int align = 16) {
     t.g_cols = g;
     t.nm = g / t.n_mma;
     t.acc_stages = (2 * g <= 512) ? 2 : 1;
-    t.b_stage_bytes = (uint32_t)((g / 2) * kBK * 2);
+    t.stage_bytes = (uint32_t)(kBM * kBK * 2 + (g / 2) * kBK * 2);
+    int stages = (int)((kSmemLimit - 2048) / t.stage_bytes);
+    t.stages = stages > 8 ? 8 : stages;
     uint32_t cols = 32;
     while (cols < (uint32_t)(t.acc_stages * g)) cols <<= 1;
     t.tmem_cols = cols;
@@ -2364,7 +2322,10 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.nm = t.nm;
     prm.acc_stages = t.acc_stages;
     prm.k_blocks = p->k_pad / kBK;
-    prm.b_stage_bytes = t.b_stage_bytes;
+    prm.stages = t.stages;
+    prm.stage_bytes = t.stage_bytes;
+    const uint32_t b_half = (uint32_t)(t.g_cols / 2) * kBK * 2;
+    prm.tx_bytes = 2 * (b_half + (fused ? 0u : (uint32_t)(kBM * kBK * 2)));
     prm.idesc = make_idesc_f16(2 * kBM, t.nm, c.dtype == PNCE_DTYPE_BF16);
     prm.tmem_cols = t.tmem_cols;
     prm.n_r = c.n_r;
@@ -2384,27 +2345,6 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.truth = truth;
     prm.stats = stats;
     return PNCE_OK;
-}
-
-// A/B ring depths for `budget` bytes of shared memory: B (L2-resident circulant) gets `b_def`
-// slots, A (HBM sample rows / converted stages) the rest, at most `a_max`; knobs override.
-static pnce_status_t size_rings(CorrParams& prm, int64_t budget, int a_def, int b_def, int a_max) {
-    constexpr int64_t kA = kBM * kBK * 2;
-    const Knobs& kn = knobs();
-    int sb = kn.b_stages > 0 ? kn.b_stages : b_def;
-    int sa = kn.a_stages > 0 ? kn.a_stages : (a_def > 0 ? a_def : a_max);
-    sb = (int)std::min<int64_t>(sb, (budget - 2 * kA) / prm.b_stage_bytes);
-    sa = (int)std::min<int64_t>(sa, (budget - (int64_t)sb * prm.b_stage_bytes) / kA);
-    sa = std::min(sa, 16);
-    sb = std::min(sb, 8);
-    if (sa < 2 || sb < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the A/B rings");
-    prm.a_stages = sa;
-    prm.b_stages = sb;
-    return PNCE_OK;
-}
-
-static size_t ring_bytes(const CorrParams& prm) {
-    return (size_t)prm.a_stages * (kBM * kBK * 2) + (size_t)prm.b_stages * prm.b_stage_bytes;
 }
 
 static int pair_grid(const pnce_plan_t* p, const CorrParams& prm) {
@@ -2466,14 +2406,11 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
         s = scored_prepare(p, res, n_frames, st, prm);
         if (s != PNCE_OK) return s;
     }
-    // packed operand: 6 A slots (HBM rows) + 4 B slots (A/B measured: 6/4 ~ coupled 4 stages,
-    // 8/3 and 4/4 slower); the LDG variant keeps 3 B slots and gives the rest to A
-    s = ldg ? size_rings(prm, (int64_t)kSmemLimit - 2048, -1, 3, 12) : size_rings(prm, (int64_t)kSmemLimit - 2048, 6, 4, 6);
-    if (s != PNCE_OK) return s;
     if (ldg) {
         prm.packed = static_cast<const uint16_t*>(packed);
         prm.packed_rows = (int64_t)packed_rows;
-        const size_t smem = 1024 + ring_bytes(prm) + 1024;
+        prm.tx_bytes = 2 * (uint32_t)(t.g_cols / 2) * kBK * 2;  // circulant only
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         launch_k3<kModePackedLdg>(scored, pair_grid(p, prm), smem, st, t.tm_circ, t.tm_circ, prm);
     } else {
         const uint64_t key[3] = {packed_rows, (uint64_t)p->k_pad, 1};
@@ -2486,7 +2423,7 @@ pnce_status_t pnce_correlate(const pnce_plan_t* p, const void* packed, float* ta
             res->tm_in_ptr = packed;
             std::memcpy(res->tm_in_key, key, sizeof(key));
         }
-        const size_t smem = 1024 + ring_bytes(prm) + 1024;
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         launch_k3<kModePacked>(scored, pair_grid(p, prm), smem, st, res->tm_in, t.tm_circ, prm);
     }
     g_launches++;
@@ -2672,18 +2609,18 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.truth_slots = kn.truth_slots;
             budget -= (int64_t)epi_warps * prm.truth_slots * 2048;
         }
-        // rings: A (converted stages) and B (circulant) slots, the rest of the shared memory
-        // for the raw half-K-block ring (its depth sets the HBM reads in flight)
-        s = size_rings(prm, budget - 2 * (int64_t)prm.raw_stage_bytes, 3, 3, 3);
-        if (s != PNCE_OK) return s;
-        int raw = (int)std::min<int64_t>(12, (budget - (int64_t)ring_bytes(prm)) / prm.raw_stage_bytes);
+        int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
+        if (kn.ab_stages > 0) ab = std::min<int>((int)(budget / prm.stage_bytes), kn.ab_stages);
+        int raw = (int)std::min<int64_t>(8, (budget - (int64_t)ab * prm.stage_bytes) / prm.raw_stage_bytes);
         if (kn.raw_stages > 0) raw = std::min(raw, kn.raw_stages);
-        if (raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        if (ab < 2 || raw < 2) return fail(PNCE_ERR_INVALID_CONFIG, "shared memory too small for the fused pipeline");
+        prm.stages = ab;
         prm.raw_stages = raw;
         // one scratch slot is enough when a K-block's store for row tile r+1 (group 0) comes at
-        // least `a_stages` jobs after the last group's load of it for row tile r: k_blocks >= a_stages
-        if (prm.a_reuse && prm.k_blocks < prm.a_stages) prm.scr_slots = 2;
-        prm.truth_off = (uint32_t)(ring_bytes(prm) + prm.bar_bytes + (size_t)prm.raw_stages * prm.raw_stage_bytes);
+        // least `stages` jobs after the last group's load of it for row tile r: k_blocks >= stages
+        if (prm.a_reuse && prm.k_blocks < prm.stages) prm.scr_slots = 2;
+        prm.truth_off = (uint32_t)((size_t)prm.stages * prm.stage_bytes + prm.bar_bytes +
+                                   (size_t)prm.raw_stages * prm.raw_stage_bytes);
         const size_t smem = 1024 + (size_t)prm.truth_off + (size_t)epi_warps * prm.truth_slots * 2048;
         const int grid = pair_grid(p, prm);
         if (prm.a_reuse) {
@@ -2726,9 +2663,8 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
                                      prm.a_reuse ? &res->tm_scr : nullptr);
         }
     } else {
-        s = size_rings(prm, (int64_t)kSmemLimit - 2048, -1, 3, 12);
-        if (s != PNCE_OK) return s;
-        const size_t smem = 1024 + ring_bytes(prm) + 1024;
+        if (kn.ab_stages > 0) prm.stages = std::min(prm.stages, std::max(2, kn.ab_stages));
+        const size_t smem = 1024 + (size_t)prm.stages * prm.stage_bytes + 1024;
         // the LDG variant reads the rows directly (tm_in unused; the circulant map fills the slot)
         launch_k3<kModeFusedLdg>(scored, pair_grid(p, prm), smem, st, tiling.tm_circ, tiling.tm_circ, prm);
     }
