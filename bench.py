@@ -30,6 +30,11 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json configs[2] (headline single-GPU bench)
 WORKLOAD = dict(name="cfg3", n_t=64, n_r=64, m=1023, l=64, c=64, n_batch=8, snr_db=10.0)
+# the `config` object both arms print, textually identical (the per-step sample sizes and the
+# parallelism of each arm are reported beside it, under "run")
+CONFIG = {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8, 10 dB (BASELINE configs[2])",
+          "metric_unit": "CSI estimates/s (link CIRs of L taps per second)",
+          "l2": "GPU arm: inputs (f32 IQ, 4.7 MB per frame-set) far larger than the 126 MB L2, no flush"}
 def _baseline_metric() -> str:
     """BASELINE.json's metric string, verbatim (fallback: the same text)."""
     try:
@@ -209,8 +214,9 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": med * 1e3, "us_per_frame": med * 1e6, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8, 10 dB",
-                   "frames_per_step": 1, "parallelism": "host threads (OpenBLAS)"},
+        "config": dict(CONFIG),
+        "run": {"frames_per_step": 1, "parallelism": "host threads (OpenBLAS)",
+                "sample": "each step: the median of a bounded sample of cfg3 frame-sets (--ref-seconds)"},
         "cpu_baseline": {"value": value, "unit": "CSI estimates/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "CSI estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -360,10 +366,18 @@ def run_gpu(args, rank, world):
     stream = torch.cuda.current_stream(dev)
     L = _lib.lib()
 
+    launch_frames = args.launch_frames if args.launch_frames > 0 else F
+    iq_stride = iq[0].numel() * 4 if F > 0 else 0
+    taps_stride = taps[0].numel() * 8 if F > 0 else 0
+
     def step():
-        # the hot path: ONE fused launch (CP strip + quantise + tcgen05 correlate + demux + 1/M)
-        _lib.check(L.pnce_process_frames(corr._plan, iq.data_ptr(), taps.data_ptr(), None, None, None, 0, F,
-                                         stream.cuda_stream))
+        # the hot path: fused launches (CP strip + quantise + tcgen05 correlate + demux + 1/M),
+        # one per `launch_frames` frame-sets (default: ONE launch over all F)
+        for f0 in range(0, F, launch_frames):
+            n = min(launch_frames, F - f0)
+            _lib.check(L.pnce_process_frames(corr._plan, iq.data_ptr() + f0 * iq_stride,
+                                             taps.data_ptr() + f0 * taps_stride, None, None, None, 0, n,
+                                             stream.cuda_stream))
 
     for _ in range(args.warmup):
         step()
@@ -590,9 +604,8 @@ def run_gpu(args, rank, world):
             "dtype": args.dtype,
             "data": f"synthetic: {F} distinct frame-sets from the device synthesiser (draw_channel law, "
                     f"pilot sweep, {w['snr_db']:g} dB AWGN; {synth_s:.2f} s, untimed)",
-            "config": {"workload": "cfg3 64x64 MIMO, PN 1023, L=C=64, N_batch=8 (BASELINE configs[2])",
-                       "frames_per_step": F, "input_bytes_per_step": iq.numel() * 4,
-                       "l2": "inputs (47 GB f32 IQ at 10k frames) >> 126 MB L2; no flush needed",
+            "config": dict(CONFIG),
+            "run": {"frames_per_step": F, "launch_frames": launch_frames, "input_bytes_per_step": iq.numel() * 4,
                        "parallelism": f"dp{world} (frames sharded, no hot-path collective)",
                        "dist_backend": args.dist_backend if world > 1 else None,
                        "distinct_devices": min(world, torch.cuda.device_count())},
@@ -642,6 +655,7 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend under torchrun (gloo: several ranks may share one GPU)")
     ap.add_argument("--antenna-reps", type=int, default=50, help="antenna-sharded latency samples (0: off)")
+    ap.add_argument("--launch-frames", type=int, default=0, help="frame-sets per fused launch in a step (0: all)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

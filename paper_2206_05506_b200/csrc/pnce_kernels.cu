@@ -253,6 +253,22 @@ __global__ void k_pack_iq(const float* __restrict__ iq, T* __restrict__ out, int
 //   4-11 converters (fused)                          12-15 epilogue (one per TMEM lane quarter)
 enum { kModePacked = 0, kModeFusedLdg = 1, kModeFusedTma = 2, kModePackedLdg = 3 };
 
+#ifdef PNCE_DIAG_CHECKS
+// Diagnostic build: device-side bounds checks on every global / shared access of the kernels
+// (compute-sanitizer is not available on the GPU pool); a violation prints and traps.
+#define PNCE_CHECK(cond)                                                                               \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("PNCE_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define PNCE_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 #ifdef PNCE_DIAG_TRACE
 // Diagnostic timeline (globaltimer ns) for the first CTA pair: [cta][slot][index].
 constexpr int kTraceSlots = 16, kTraceMax = 512;
@@ -341,6 +357,10 @@ struct CorrParams {
     int32_t chunk_kb;    // K-blocks per accumulation unit (= k_blocks outside tensor16 mode)
     int32_t acc16;       // 1: binary16 partials (F16 TMEM accumulator), 0: binary32
     uint32_t* sat_flags; // tensor16: [F][n_batches] set when a partial / total is non-finite
+    // bounds of the caller's buffers (PNCE_DIAG_CHECKS builds)
+    int64_t n_taps;      // complex taps in `taps` (and `truth`): F n_r n_t L
+    int64_t n_frames;    // F
+    int64_t scr_rows;    // rows of the a_reuse scratch
 };
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, int bf16) {
@@ -420,8 +440,10 @@ __device__ __forceinline__ void link_flush(const CorrParams& p, const EpiLink& e
         v += __shfl_xor_sync(0xffffffffu, v, 1);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
     }
-    if ((!quad || (threadIdx.x & 3) == 0) && e.out >= 0 && a.w >= 0 && v != 0.f)
+    if ((!quad || (threadIdx.x & 3) == 0) && e.out >= 0 && a.w >= 0 && v != 0.f) {
+        PNCE_CHECK(e.lbase + a.w < p.n_taps / p.l && a.w < p.n_batch);
         atomicAdd(p.link_err + e.lbase + a.w, v * p.inv_l);
+    }
     a.part = 0.f;
 }
 
@@ -458,6 +480,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
 #endif
         float* dst = p.taps + 2 * (e.out + lag);
         const float* tr = p.truth + 2 * (e.out + lag);
+        PNCE_CHECK(e.out + lag >= 0 && e.out + lag + (lag + 1 < e.n_valid ? 1 : 0) < p.n_taps);
         if (lag + 1 < e.n_valid) {
             if (SC && p.stats != nullptr) {
                 nf = fmaf(re1, 0.f, nf);
@@ -570,6 +593,7 @@ __device__ __forceinline__ void epi_reps_scored(const CorrParams& p, const uint3
         if (e.out < 0 || lag >= e.n_valid) continue;
         // (non-finite taps show up in s_sq: the caller flags a recount from it, see below)
         float* dst = p.taps + 2 * (e.out + lag);
+        PNCE_CHECK(e.out + lag >= 0 && e.out + lag + (lag + 1 < e.n_valid ? 1 : 0) < p.n_taps);
         const float q0 = err_acc(re0, im0, h[i].x, h[i].y, s_abs, s_sq);
         if (lag + 1 < e.n_valid) {
             if (e.vec) {
@@ -643,6 +667,7 @@ __device__ __forceinline__ void epi_block_scored_smem(const CorrParams& p, uint3
                 const bool ok = e.out >= 0 && lag < e.n_valid;
                 const uint32_t bytes = ok ? (lag + 1 < e.n_valid ? 16u : 8u) : 0u;
                 const float* src = ok ? p.truth + 2 * (e.out + lag) : p.truth;
+                PNCE_CHECK(!ok || (e.out + lag + (bytes == 16u ? 1 : 0) < p.n_taps));
                 cp_async_16(ring + (uint32_t)(((slot * 4 + i) * 32 + lane) * 16), src, bytes);
             }
         }
@@ -692,6 +717,7 @@ __device__ __forceinline__ void epi_reps_fast(const uint32_t* v, float* dst, flo
 
 __device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst, int cols) {
     const float s = p.inv_m;
+    PNCE_CHECK(dst >= p.taps && dst + 2 * cols - 12 <= p.taps + 2 * p.n_taps);  // last 16-byte store of the thread
     const uint64_t pol = p.store_hint ? policy_evict_first() : 0ull;
     int c = 0;
     uint32_t va[32], vb[32];
@@ -771,6 +797,7 @@ __device__ __forceinline__ void t16_fold(const CorrParams& p, uint32_t t_part, u
                 if (lag >= e.n_valid) continue;
                 if (!(isfinite(re0) && isfinite(im0))) sat = true;
                 float* dst = p.taps + 2 * (e.out + lag);
+                PNCE_CHECK(e.out + lag >= 0 && e.out + lag + (lag + 1 < e.n_valid ? 1 : 0) < p.n_taps);
                 if (lag + 1 < e.n_valid) {
                     if (!(isfinite(re1) && isfinite(im1))) sat = true;
                     if (e.vec) {
@@ -851,6 +878,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
+    if (threadIdx.x == 0) TRACE(13, 0);  // kernel entry
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -884,6 +912,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TRACE(14, 0);  // prologue done
 
     const int n_clusters = gridDim.x >> 1;
     const int cid = blockIdx.x >> 1;
@@ -904,7 +933,9 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     };
     // scratch row of (row-tile iteration r, this CTA, K-block kb); slots alternate per row tile
     auto scr_row = [&](int r, int kb) -> int {
-        return ((((r % p.scr_slots) * n_clusters + cid) * 2 + (int)rank) * p.k_blocks + kb) * kBM;
+        const int row = ((((r % p.scr_slots) * n_clusters + cid) * 2 + (int)rank) * p.k_blocks + kb) * kBM;
+        PNCE_CHECK(row >= 0 && row + kBM <= p.scr_rows);
+        return row;
     };
     const int jobs = my_tiles * p.k_blocks;  // one job = one K-block of one tile
     const uint32_t a_bytes = kBM * kBK * 2;
@@ -1186,6 +1217,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             const int idx = cw + kCW * it;  // 0..31
                             const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
                             const uint32_t src = raw + link * (p.raw_row_floats * 4);
+                            PNCE_CHECK(src + 16 <= smem_u32(raw_base + (size_t)(rs + 1) * p.raw_stage_bytes));
                             if (slack == 0) {
                                 v[it] = ld_shared_v4f(src);
                             } else {
@@ -1198,6 +1230,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         for (int it = 0; it < kIt; ++it) {
                             const int idx = cw + kCW * it;
                             const int link = (idx & 3) | ((lane >> 4) << 2) | ((idx >> 2) << 3);
+                            PNCE_CHECK(swz(sa, (int)a_row(link, 1), col_byte) + 4 <= sa + kBM * kBK * 2);
                             if (!ok0) { v[it].x = 0.f; v[it].y = 0.f; }
                             if (!ok1) { v[it].z = 0.f; v[it].w = 0.f; }
                             st_shared_u32(swz(sa, (int)a_row(link, 0), col_byte), pack2(v[it].x, v[it].z, p.bf16));
@@ -1327,6 +1360,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                 for (int q = 0; q < kLinksPerTile / 4; ++q) {
                     // link 4q + gw of the tile; lane -> samples 2*lane, 2*lane+1 (one 128 B row)
                     const int link_local = 4 * q + gw;
+                    PNCE_CHECK(swz(sa, (int)a_row(link_local, 1), lane * 4) + 4 <= sa + kBM * kBK * 2);
                     st_shared_u32(swz(sa, (int)a_row(link_local, 0), lane * 4), pack2(v[q].x, v[q].z, p.bf16));
                     st_shared_u32(swz(sa, (int)a_row(link_local, 1), lane * 4), pack2(v[q].y, v[q].w, p.bf16));
                 }
@@ -1600,6 +1634,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             bad += __shfl_xor_sync(0xffffffffu, bad, o);
                         }
                         if (lane == 0 && lead_ok) {
+                            PNCE_CHECK(f0 >= 0 && f0 < p.n_frames);
                             if (p.truth != nullptr) {
                                 atomicAdd(&p.stats[f0 * 4 + 0], (double)sa);
                                 atomicAdd(&p.stats[f0 * 4 + 1], (double)sq);
@@ -1607,6 +1642,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             if (bad != 0.f) atomicAdd(&p.stats[f0 * 4 + 2], (double)bad);
                         }
                     } else if (e.out >= 0) {
+                        PNCE_CHECK(e.f >= 0 && e.f < p.n_frames);
                         if (p.truth != nullptr) {
                             atomicAdd(&p.stats[e.f * 4 + 0], (double)sa);
                             atomicAdd(&p.stats[e.f * 4 + 1], (double)sq);
@@ -1622,6 +1658,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
     __syncwarp();
     tc_fence_before();
     cluster_sync_all();
+    if (threadIdx.x == 0) TRACE(15, 0);  // all roles done
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_pair(tmem_base, p.tmem_cols);
@@ -2344,6 +2381,8 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.taps = taps;
     prm.truth = truth;
     prm.stats = stats;
+    prm.n_frames = n_frames;
+    prm.n_taps = n_frames * (int64_t)c.n_r * c.n_t * c.l;
     return PNCE_OK;
 }
 
@@ -2638,6 +2677,7 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
                 res->tm_scr_rows = rows;
             }
             prm.scratch = res->scratch;
+            prm.scr_rows = (int64_t)rows;
         }
         if (t16) {
             const int64_t n_fb = n_frames * p->n_batches;
