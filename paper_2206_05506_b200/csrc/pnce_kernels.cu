@@ -324,7 +324,7 @@ struct CorrParams {
     int32_t raw_stages;      // FusedTma: f32 staging ring depth (half-K-block chunks)
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
-    int32_t store_hint;   // taps stores with an L2 evict_first policy (default; 0 via knob)
+    int32_t store_hint;   // L2 policy of the taps stores: 1 evict_first (default), 2 evict_last, 3 normal, 0 none
     int32_t raw_pol;      // L2 policy of the raw f32 row loads: 0 evict_first, 1 normal, 2 evict_last
     int32_t a_reuse;      // FusedTma, n_groups > 1: group 0 converts once and stores the fp16 A
                           // stages to `scratch`; the other groups of the row tile TMA them back
@@ -718,7 +718,10 @@ __device__ __forceinline__ void epi_reps_fast(const uint32_t* v, float* dst, flo
 __device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst, int cols) {
     const float s = p.inv_m;
     PNCE_CHECK(dst >= p.taps && dst + 2 * cols - 12 <= p.taps + 2 * p.n_taps);  // last 16-byte store of the thread
-    const uint64_t pol = p.store_hint ? policy_evict_first() : 0ull;
+    const uint64_t pol = p.store_hint == 1   ? policy_evict_first()
+                         : p.store_hint == 2 ? policy_evict_last()
+                         : p.store_hint == 3 ? policy_evict_normal()
+                                             : 0ull;
     int c = 0;
     uint32_t va[32], vb[32];
     if (cols >= 64) {
