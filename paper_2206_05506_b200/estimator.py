@@ -356,6 +356,22 @@ class Correlator:
         cur.wait_stream(s_out)
         return taps_host
 
+    def capture(self, iq: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.cuda.CUDAGraph, torch.Tensor]:
+        """Record `process(iq, out)` into a CUDA graph for repeated calls on the same buffers
+        (the real-time single frame-set case): `graph.replay()` re-runs the fused launch with
+        one cudaGraphLaunch instead of the Python + C-ABI launch path.  Refill `iq` in place
+        between replays; the taps land in the returned `out`."""
+        iq, n_frames = self._check_iq(iq)
+        if out is None:
+            out = torch.empty(self.taps_shape(n_frames), dtype=torch.complex64, device=self.device)
+        with torch.cuda.device(self.device):
+            self.process(iq, out=out)                 # warm: the capture stream's resources
+            torch.cuda.synchronize(self.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self.process(iq, out=out)
+        return graph, out
+
     def pack(self, iq: torch.Tensor) -> torch.Tensor:
         """K2 alone: returns the packed 16-bit operand (K_pad columns; rows in 16-row blocks of
         8 links, Re rows then Im rows -- see pnce_workspace_bytes in include/pnce_b200.h)."""

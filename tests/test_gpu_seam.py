@@ -192,3 +192,21 @@ def test_streams_share_a_plan(dev):
     torch.cuda.synchronize(dev)
     for o in outs:
         assert torch.equal(o, ref)
+
+
+def test_graph_capture_replays_the_fused_launch(dev):
+    """Correlator.capture: a CUDA graph of the fused launch gives the same taps on replay,
+    also after the input buffer is refilled in place."""
+    cfg, _, _, iq, _ = cfg2_sets(2)
+    corr = P.Correlator(P.default_spec(8), cfg, 16, device=dev)
+    x = torch.from_numpy(iq[:1]).to(dev).contiguous()
+    graph, out = corr.capture(x)
+    want0, _ = corr.process(x)
+    graph.replay()
+    torch.cuda.synchronize(dev)
+    assert torch.equal(out, want0)
+    x.copy_(torch.from_numpy(iq[1:2]))
+    graph.replay()
+    torch.cuda.synchronize(dev)
+    want1, _ = corr.process(x)
+    assert torch.equal(out, want1) and not torch.equal(want0, want1)
