@@ -14,7 +14,7 @@ for r in rows[1:]:
         continue
     name = re.sub(r"<unnamed>::", "", r[k_i]).split("(")[0]
     if not any(k in name for k in ("k_lfsr", "k_build_circulant", "k_pack_iq", "k_correlate", "k_t16_finish",
-                                   "k_draw_channel", "k_synth")):
+                                   "k_sat_finish", "k_draw_channel", "k_synth", "k_h_split", "k_build_bsyn")):
         continue
     agg.setdefault(name, []).append(float(r[v_i].replace(",", "")) / 1000.0)
 tot = sum(sum(v) for v in agg.values())
