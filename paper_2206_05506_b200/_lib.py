@@ -91,6 +91,8 @@ def lib() -> ctypes.CDLL:
         "pnce_kernel_launches": (i64, []),
     }
     for name, (res, args) in sig.items():
+        if "PNCE_LIB" in os.environ and not hasattr(L, name):
+            continue  # diagnostic override library (tools/bin) built from an older revision
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
