@@ -38,7 +38,10 @@ CSV_COLUMNS = ("experiment", "backend", "nt", "nr", "m", "c", "l", "l_nz", "n_ba
 
 @dataclass(frozen=True)
 class ExperimentConfig:
-    """experiments.py:45-80 (backend = operand dtype of the device path)."""
+    """experiments.py:45-80.  ``backend``: "fp16" / "bf16" (operand dtype of the fused path) or
+    the reference's ``BackendConfig`` (backend.py): reference64/32 run the fused fp16 path,
+    tensor16 runs the tensor16 mode with its chunk_len / accumulator (the paper's §III-B
+    precision study on real tensor cores); the CSV backend column is then the kind."""
 
     n_t: int = 16
     n_r: int = 16
@@ -50,7 +53,7 @@ class ExperimentConfig:
     snr_db: tuple[float, ...] = DEFAULT_SNR_GRID_DB
     iterations: int = 50
     seed: int = 0
-    backend: str = "fp16"
+    backend: object = "fp16"
     f_s: float = 10e6
     emit_per_iteration: bool = False
     record_latency: bool = True
@@ -183,15 +186,21 @@ def _gather_rows(indexed_rows: list[tuple[int, list[SweepResult]]], group=None) 
 _CORR_CACHE: dict = {}
 
 
+def _mode(cfg: ExperimentConfig):
+    from .backend import resolve
+    return resolve(cfg.backend)
+
+
 def _correlator(cfg: ExperimentConfig, m: int, n_batch: int, device: torch.device):
     from .estimator import Correlator
     from .pilots import PilotConfig
     from .pn import default_spec
-    key = (m, n_batch, cfg.n_t, cfg.n_r, cfg.c, cfg.l, cfg.backend, str(device))
+    dtype = _mode(cfg).dtype
+    key = (m, n_batch, cfg.n_t, cfg.n_r, cfg.c, cfg.l, dtype, str(device))
     if key not in _CORR_CACHE:
         pilot = PilotConfig(m=m, c=cfg.c, n_t=cfg.n_t, n_batch=n_batch, l=cfg.l, f_s=cfg.f_s)
         _CORR_CACHE[key] = Correlator(default_spec((m + 1).bit_length() - 1), pilot, cfg.n_r,
-                                      dtype=cfg.backend, device=device)
+                                      dtype=dtype, device=device)
     return _CORR_CACHE[key]
 
 
@@ -234,8 +243,12 @@ def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device,
             synth.simulate_frames(corr, h[it:it + 1], pt.snr_db, seed=ns, out=iq[it:it + 1])
     stream = torch.cuda.current_stream(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mode = _mode(cfg)
     ev0.record(stream)
-    _, stats, _ = corr.process_scored(iq, h)
+    if mode.tensor16:   # zeroed + counted saturated batches, sums over the returned taps
+        _, stats = corr.process_tensor16(iq, chunk_len=mode.chunk_len, accumulator=mode.accumulator, truth=h)
+    else:
+        _, stats, _ = corr.process_scored(iq, h)
     ev1.record(stream)
     torch.cuda.synchronize(device)
     per_frame = (ev0.elapsed_time(ev1) / 1e3) / it_n if cfg.record_latency else 0.0
@@ -245,7 +258,7 @@ def evaluate_point(cfg: ExperimentConfig, pt: SweepPoint, device: torch.device,
     pil = corr.cfg
     samples_moved = pil.n_batches * cfg.n_r * pil.p
     macs = cfg.n_t * cfg.l * pt.m * cfg.n_r
-    backend = f"tcgen05-{cfg.backend}"
+    backend = mode.kind
 
     def row(name, iters, seed, mae_v, lat, sat):
         return SweepResult(name, backend, cfg.n_t, cfg.n_r, pt.m, cfg.c, cfg.l, pt.l_nz, pt.n_batch, pt.snr_db,
@@ -328,13 +341,17 @@ def run_latency_bench(cfg: ExperimentConfig, reps: int = 10, warmup: int = 2, de
             for rep in range(warmup + reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(torch.cuda.current_stream(device))
-                corr.process(iq, out=taps)
+                if _mode(cfg).tensor16:
+                    m16 = _mode(cfg)
+                    corr.process_tensor16(iq, chunk_len=m16.chunk_len, accumulator=m16.accumulator, out=taps)
+                else:
+                    corr.process(iq, out=taps)
                 e1.record(torch.cuda.current_stream(device))
                 torch.cuda.synchronize(device)
                 if rep >= warmup:
                     times.append(e0.elapsed_time(e1) / 1e3)
             pil = corr.cfg
-            points.append(BenchPoint(f"tcgen05-{cfg.backend}", cfg.n_t, cfg.n_r, m, cfg.c, cfg.l, cfg.l_nz[0], nb,
+            points.append(BenchPoint(_mode(cfg).kind, cfg.n_t, cfg.n_r, m, cfg.c, cfg.l, cfg.l_nz[0], nb,
                                      cfg.snr_db[0], len(times), statistics.fmean(times),
                                      statistics.stdev(times) if len(times) > 1 else 0.0, statistics.median(times),
                                      pil.n_batches * cfg.n_r * pil.p, cfg.n_t * cfg.l * m * cfg.n_r, cfg.seed,

@@ -121,3 +121,26 @@ def test_latency_bench_rows(dev):
     assert rows[0].macs == 16 * 32 * 255 * 16 and rows[0].samples_moved == 16 * 16 * (32 + 255)
     text = SW.render_csv(rows)
     assert SW.render_csv(SW.parse_csv(text)) == text
+
+
+def test_tensor16_sweep_matches_reference_csv(dev):
+    """The reference's tensor16 sweep (BackendConfig(kind="tensor16", chunk_len=128,
+    accumulator="binary16"), the paper's precision study) run on the tensor cores with the
+    reference's own frames: same rows, backend column "tensor16", counters and saturations
+    exact, every per-iteration MAE within 0.05 dB of the real reference's emulation
+    (tests/golden/ref_t16_sweep.csv)."""
+    from paper_2206_05506_b200.backend import BackendConfig
+    with open(os.path.join(GOLD, "ref_t16_sweep.csv"), newline="") as fh:
+        ref = SW.parse_csv(fh.read())
+    cfg = SW.ExperimentConfig(n_t=16, n_r=16, pn_lengths=(255,), c=32, l=32, l_nz=(32,), n_batch=(4,),
+                              snr_db=(0.0, 15.0, 30.0), iterations=6, seed=0, emit_per_iteration=True,
+                              record_latency=False,
+                              backend=BackendConfig(kind="tensor16", chunk_len=128, accumulator="binary16"))
+    rows = SW.run_snr_sweep(cfg, device=dev, frame_source=oracle_source)
+    assert len(rows) == len(ref) == 3 * 7
+    worst = 0.0
+    for a, b in zip(rows, ref):
+        assert (a.experiment, a.backend, a.snr_db, a.iterations, a.seed, a.samples_moved, a.macs, a.saturations) == \
+               (b.experiment, b.backend, b.snr_db, b.iterations, b.seed, b.samples_moved, b.macs, b.saturations)
+        worst = max(worst, db(a.mae, b.mae))
+    assert worst <= 0.05, worst
