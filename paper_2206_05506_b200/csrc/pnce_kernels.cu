@@ -64,7 +64,7 @@ std::atomic<int64_t> g_launches{0};
 struct Knobs {
     int epi8, group_fused, group_packed, group_packed_ldg, t16_g, narrow_g;
     int store_hint, raw_pol, split_drain, packed_mode, scored_g, narrow, mid, fused_mode, narrow_ldg;
-    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi, t16_epi;
+    int a_reuse, scr_pol, scr_slots, truth_slots, ab_stages, raw_stages, scored_epi, t16_epi, wide_ldg;
 };
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -97,6 +97,7 @@ const Knobs& knobs() {
         r.raw_stages = env_int("PNCE_TUNE_RAW_STAGES", -1);
         r.scored_epi = env_int("PNCE_TUNE_SCORED_EPI", 8);
         r.t16_epi = env_int("PNCE_TUNE_T16_EPI", 8);
+        r.wide_ldg = env_int("PNCE_TUNE_WIDE_LDG", 1);
         return r;
     }();
     return k;
@@ -2613,6 +2614,13 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     // frame-set, bit-identical (tools/narrow_mode_trial.sh; PNCE_TUNE_NARROW_LDG=0: TMA ring)
     if (narrow && kn.fused_mode < 0 && kn.narrow_ldg == 1) use_tma = false;
     if (mid && kn.fused_mode < 0 && kn.mid == 2) use_tma = false;
+    // plain launches with >= 3 lag-row groups (cfg4': R = 2032, K = 2048) are MMA-bound: the LDG
+    // converters (no raw TMA boxes queued ahead of the circulant loads in the TMA engine) beat the
+    // TMA raw ring + A-stage reuse, 14.9 vs 15.9 us per cfg4' frame-set, bit-identical
+    // (tools/cfg4_probe6.sh; PNCE_TUNE_WIDE_LDG=0: TMA ring).  Scored launches keep the ring
+    // (27 vs 37 us: the truth ring needs its shared memory).
+    if (!t16 && !scored && kn.fused_mode < 0 && kn.wide_ldg == 1 && tiling.n_groups >= 3 && !narrow && !mid)
+        use_tma = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     StreamRes* res = stream_res(const_cast<pnce_plan*>(p), st);
     if (scored && stats) s_ok_or_return(scored_prepare(p, res, n_frames, st, prm));

@@ -1,7 +1,8 @@
 """Pipeline variants that must not change a single bit: the split drain (first accumulator
 half released early), the A-stage reuse across lag-row groups (L2 scratch), and the
 LDGSTS truth ring of the scored drain, the narrow lag-row groups of few-tile launches and
-their LDG converters, the 256-column tiling of 5-9 frame-set launches --
+their LDG converters, the 256-column tiling of 5-9 frame-set launches, the LDG converters
+of plain launches with >= 3 groups (cfg4') --
 each run in a subprocess with its knob off and
 compared with the default build of the same launch (same MMAs in the same K order, same
 epilogue arithmetic).  Covers one group (cfg3), two groups (scored / tensor16 tilings) and
@@ -65,7 +66,7 @@ def default_run(tmp_path_factory):
                                         ("PNCE_TUNE_TRUTH_SLOTS", "0"), ("PNCE_TUNE_TRUTH_SLOTS", "3"),
                                         ("PNCE_TUNE_NARROW", "0"), ("PNCE_TUNE_NARROW_LDG", "0"), ("PNCE_TUNE_MID", "0"),
                                         ("PNCE_TUNE_SCORED_G", "256"), ("PNCE_TUNE_SCORED_EPI", "4"),
-                                        ("PNCE_TUNE_T16_EPI", "4")])
+                                        ("PNCE_TUNE_T16_EPI", "4"), ("PNCE_TUNE_WIDE_LDG", "0")])
 def test_variant_bit_identical(default_run, tmp_path, knob, value):
     other = _run(tmp_path, knob + value, {knob: value})
     for key in default_run.files:

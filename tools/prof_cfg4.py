@@ -13,11 +13,21 @@ corr = P.Correlator(P.default_spec(11), cfg, 128, device=dev)
 h = S.draw_channel(corr, F, seed=77)
 iq = S.simulate_frames(corr, h, 10.0, seed=78)
 taps = torch.empty(corr.taps_shape(F), dtype=torch.complex64, device=dev)
+mode = sys.argv[2] if len(sys.argv) > 2 else "fused"
+if mode == "packed":  # the GEMM on the packed fp16 operand instead
+    packed = corr.pack(iq)
+    run = lambda: corr.correlate(packed, F, out=taps)  # noqa: E731
+elif mode == "scored":  # fused + per-frame sums and per-link MSE against the drawn channel
+    stats = torch.zeros((F, 4), dtype=torch.float64, device=dev)
+    link = torch.zeros((F, 128, 128), dtype=torch.float32, device=dev)
+    run = lambda: corr.process_scored(iq, h, out=taps, stats=stats, link_mse=link)  # noqa: E731
+else:
+    run = lambda: corr.process(iq, out=taps)  # noqa: E731
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for _ in range(3):
-    corr.process(iq, out=taps)
+    run()
 e0.record()
-corr.process(iq, out=taps)
+run()
 e1.record()
 torch.cuda.synchronize()
-print(f"cfg4' fused {e0.elapsed_time(e1) * 1e3 / F:.2f} us/frame-set")
+print(f"cfg4' {mode} {e0.elapsed_time(e1) * 1e3 / F:.2f} us/frame-set")
