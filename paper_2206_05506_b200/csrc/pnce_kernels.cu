@@ -2659,7 +2659,9 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
             prm.truth_slots = kn.truth_slots;
             budget -= (int64_t)epi_warps * prm.truth_slots * 2048;
         }
-        int ab = (int)std::min<int64_t>(3, budget / (int64_t)prm.stage_bytes);
+        // tensor16's 32 KB stages (256-column groups): 4 A/B stages, 2.85 -> 2.76 us per cfg3
+        // frame-set (5: same, 6: 2.91 -- the raw ring gets too short; tools/t16_probe.sh)
+        int ab = (int)std::min<int64_t>(t16 ? 4 : 3, budget / (int64_t)prm.stage_bytes);
         if (kn.ab_stages > 0) ab = std::min<int>((int)(budget / prm.stage_bytes), kn.ab_stages);
         int raw = (int)std::min<int64_t>(8, (budget - (int64_t)ab * prm.stage_bytes) / prm.raw_stage_bytes);
         if (kn.raw_stages > 0) raw = std::min(raw, kn.raw_stages);
