@@ -2644,7 +2644,12 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
         int64_t budget = (int64_t)kSmemLimit - 2048;
         // a_reuse (several lag-row groups): convert a row tile once, keep its fp16 A stages in an
         // L2-resident scratch for the other groups (PNCE_TUNE_A_REUSE=0: convert per group)
-        if (kn.a_reuse == 1 && !narrow && !mid && tiling.n_groups > 1 && prm.k_blocks <= 64) {
+        // (two groups: tensor16 -- 2.76 vs 2.82 us; with >= 3 groups (cfg4') the re-reads of
+        // the raw rows hit L2 (neighbouring clusters take the other groups of the same row tile)
+        // and skipping the scratch is faster: scored cfg4' 27.8 -> 25.4 us.  PNCE_TUNE_A_REUSE:
+        // 0 never, 1 two groups, 2 any number of groups)
+        if (kn.a_reuse >= 1 && !narrow && !mid && tiling.n_groups > 1 && (tiling.n_groups == 2 || kn.a_reuse == 2) &&
+            prm.k_blocks <= 64) {
             prm.a_reuse = 1;
             prm.scr_pol = kn.scr_pol;
             prm.scr_slots = kn.scr_slots > 0 ? std::max(1, std::min(2, kn.scr_slots)) : 1;

@@ -63,6 +63,7 @@ def default_run(tmp_path_factory):
 
 
 @pytest.mark.parametrize("knob,value", [("PNCE_TUNE_SPLIT_DRAIN", "0"), ("PNCE_TUNE_A_REUSE", "0"),
+                                        ("PNCE_TUNE_A_REUSE", "2"),
                                         ("PNCE_TUNE_TRUTH_SLOTS", "0"), ("PNCE_TUNE_TRUTH_SLOTS", "3"),
                                         ("PNCE_TUNE_NARROW", "0"), ("PNCE_TUNE_NARROW_LDG", "0"), ("PNCE_TUNE_MID", "0"),
                                         ("PNCE_TUNE_SCORED_G", "256"), ("PNCE_TUNE_SCORED_EPI", "4"),
