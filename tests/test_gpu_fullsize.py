@@ -1,0 +1,93 @@
+"""Parity at the benchmark's full size (10,000 frame-sets resident in HBM, the
+bench.py step) through size-independent properties, plus oracle spot checks:
+
+* the fused path (K3 converting the f32 rows itself) equals the two-pass path (K2 pack + K3 on
+  the packed operand) bit for bit on every one of the 10,000 frame-sets -- two independent
+  conversion routes into the same MMAs;
+* symmetry: negating the received samples negates every tap, conjugating them (Q -> -Q)
+  conjugates every tap -- exactly, since round-to-nearest-even, the products with the +-1
+  circulant and the fp32 sums are all sign-symmetric (the real circulant acts on I and Q
+  alike) -- on the whole 10k step;
+* the scored launch's per-frame Σ|e|² equals a device recount from the returned taps;
+* 16 frame-sets spread over the step against the oracle's reference64 estimate (per-link
+  tolerance 1e-2, the north star's).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2206_05506_b200 as P
+from paper_2206_05506_b200 import synth as S
+from oracle import pnce_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+F = 10_000
+
+
+@pytest.fixture(scope="module")
+def full():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    dev = torch.device("cuda:0")
+    cfg = P.PilotConfig(m=1023, c=64, n_t=64, n_batch=8, l=64, f_s=10e6)
+    corr = P.Correlator(P.default_spec(10), cfg, 64, device=dev)
+    iq = torch.empty(corr.iq_shape(F), dtype=torch.float32, device=dev)
+    h = torch.empty((F, 64, 64, 64), dtype=torch.complex64, device=dev)
+    for s0 in range(0, F, 1000):
+        h[s0:s0 + 1000] = S.draw_channel(corr, 1000, seed=100 + s0)
+        S.simulate_frames(corr, h[s0:s0 + 1000], 10.0, seed=200 + s0, out=iq[s0:s0 + 1000])
+    taps, _ = corr.process(iq)
+    torch.cuda.synchronize(dev)
+    yield corr, iq, h, taps
+    del iq, h, taps
+    torch.cuda.empty_cache()
+
+
+def test_fused_equals_two_pass(full):
+    corr, iq, _, taps = full
+    out = torch.empty_like(taps)
+    for s0 in range(0, F, 2500):  # the packed operand of 2,500 frame-sets at a time (5.2 GB)
+        packed = corr.pack(iq[s0:s0 + 2500])
+        corr.correlate(packed, 2500, out=out[s0:s0 + 2500])
+        del packed
+    assert torch.equal(out, taps)
+
+
+def test_sign_symmetry_full_step(full):
+    corr, iq, _, taps = full
+    iq.neg_()
+    try:
+        neg, _ = corr.process(iq)
+    finally:
+        iq.neg_()
+    assert torch.equal(neg, -taps)
+    del neg
+    iq[..., 1].neg_()
+    try:
+        conj, _ = corr.process(iq)
+    finally:
+        iq[..., 1].neg_()
+    assert torch.equal(conj, taps.conj())
+
+
+def test_scored_sums_match_recount(full):
+    corr, iq, h, taps = full
+    t2, stats, _ = corr.process_scored(iq, h)
+    assert torch.equal(t2, taps)
+    sq = ((t2 - h).abs() ** 2).double().sum(dim=(1, 2, 3))
+    torch.testing.assert_close(stats[:, 1], sq, rtol=1e-5, atol=0)
+    assert int(stats[:, 2].sum().item()) == 0 and int(stats[:, 3].sum().item()) == 0
+
+
+def test_oracle_spot_checks(full):
+    corr, iq, _, taps = full
+    ocfg = O.Config(m=1023, c=64, n_t=64, n_batch=8, l=64, n_r=64)
+    chips = O.sequence_for_length(1023)
+    rows = O.correlator_rows_for_plan(chips, O.build_batch_plan(ocfg), 64)
+    for f in np.linspace(0, F - 1, 16).astype(int):
+        ref = O.process_frames(chips, ocfg, O.iq_to_frames(iq[f].cpu().numpy()), rows_per_batch=rows)[0]
+        got = taps[f].cpu().numpy().astype(np.complex128)
+        err = np.abs(got - ref) / np.abs(ref).max(axis=-1, keepdims=True)
+        assert err.max() <= 1e-2, (int(f), float(err.max()))
