@@ -322,8 +322,32 @@ def antenna_leg(P, D, dev, stream, w, iq1, reps, rank, world):
             kern.append(k)
             tot.append(t)
     assert csi.shape == (1, w["n_r"], w["n_t"], w["l"])
+    # the same split with the all-gather fused into the epilogue: each rank's kernel stores its
+    # receivers' taps into every rank's CSI buffer (CUDA-IPC mappings, NVLink stores)
+    fused = None
+    try:
+        gat = D.CsiGather(part, w["n_r"], 1)
+        fg = []
+        for i in range(reps + 5):
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            gat.run(iq_r)
+            e1.record(stream)
+            gat.wait()
+            (t,) = D.max_over_ranks([e0.elapsed_time(e1) * 1e3])
+            if i >= 5:
+                fg.append(t)
+        fused_ok = bool(torch.equal(gat.csi, csi))
+        gat.close()
+        fused = {"us_median": st.median(fg), "csi_equal_to_allgather": fused_ok}
+    except Exception as exc:  # noqa: BLE001 -- the leg reports, the bench line survives
+        fused = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     return {"ranks": world, "receivers_per_rank": r1 - r0, "frames": 1, "reps": reps,
             "kernel_us_median": st.median(kern), "with_allgather_us_median": st.median(tot),
+            "fused_gather": fused,
             "allgather_bytes": w["n_r"] * w["n_t"] * w["l"] * 8,
             "note": "per rep: max over ranks of CUDA-event time (launch; launch + all-gather of the CIRs)"}
 

@@ -148,6 +148,19 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* plan, const float* iq, floa
                                   const float* truth, double* stats, void* workspace,
                                   size_t workspace_bytes, int64_t n_frames, void* stream);
 
+/* Antenna split with the CSI all-gather fused into the epilogue (the paper's multi-GPU
+ * scheme: N_r / N_gpu receive antennas per GPU, then Allgather() of the
+ * CIRs).  `plan` covers this rank's n_r receivers, which are rows [r0, r0 + n_r) of the
+ * n_r_total-row CSI.  Every tap is stored into `csi` (local, complex64
+ * [F][n_r_total][n_t][L]) AND into each of the n_peers (<= 7) peer buffers of the same
+ * layout (device pointers valid in this context, e.g. CUDA-IPC mappings of the other
+ * ranks' `csi`: NVLink stores from the epilogue, no separate collective).  The caller
+ * orders the ranks (stream sync + barrier) before reading the gathered CSI.  Plain
+ * estimation only (no truth/stats).  Replaces process_frames + allgather over ranks. */
+pnce_status_t pnce_process_frames_gather(const pnce_plan_t* plan, const float* iq, float* csi,
+                                         float* const* peers, int32_t n_peers, int32_t n_r_total,
+                                         int32_t r0, int64_t n_frames, void* stream);
+
 /* process_frames + fused per-link scoring (north star (4)): as pnce_process_frames,
  * and when link_err != NULL (float32 [F][n_r][n_t], zeroed by the caller; needs truth)
  * each entry receives the link's MSE, mean over its L taps of |h_est - h_true|^2,

@@ -36,7 +36,7 @@ EXPORTS = (
     "pnce_version", "pnce_last_error", "pnce_config_check", "pnce_generate_mseq",
     "pnce_plan_create", "pnce_plan_create_rows", "pnce_plan_destroy", "pnce_plan_chips", "pnce_plan_operand",
     "pnce_workspace_bytes",
-    "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored",
+    "pnce_pack_iq", "pnce_correlate", "pnce_process_frames", "pnce_process_frames_scored", "pnce_process_frames_gather",
     "pnce_process_frames_tensor16", "pnce_process_bodies_tensor16", "pnce_copy_bodies_h2d", "pnce_process_bodies", "pnce_draw_channel", "pnce_simulate_frames", "pnce_kernel_launches",
 )
 
@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         "pnce_pack_iq": (i32, [vp, vp, vp, i64, vp]),
         "pnce_correlate": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames": (i32, [vp, vp, vp, vp, vp, vp, sz, i64, vp]),
+        "pnce_process_frames_gather": (i32, [vp, vp, vp, vp, i32, i32, i32, i64, vp]),
         "pnce_process_frames_scored": (i32, [vp, vp, vp, vp, vp, vp, i64, vp]),
         "pnce_process_frames_tensor16": (i32, [vp, vp, vp, vp, vp, i32, i32, i64, vp]),
         "pnce_process_bodies_tensor16": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i64, vp]),

@@ -46,6 +46,7 @@ using namespace pnce;
 namespace {
 
 constexpr int kBM = 128;       // UMMA M (input rows per tile)
+constexpr int kMaxPeers = 7;   // peer CSI buffers of a gather launch (8 GPUs per node)
 constexpr int kBK = 64;        // K per pipeline stage (one 128B swizzle atom of 16-bit)
 constexpr int kUmmaK = 16;     // K per tcgen05.mma kind::f16
 constexpr int kSmemLimit = 227 * 1024;
@@ -325,6 +326,13 @@ struct CorrParams {
     int32_t raw_stages;      // FusedTma: f32 staging ring depth (half-K-block chunks)
     int32_t raw_row_floats;  // floats per staged link row: 64, +4 slack when C is odd
     uint32_t raw_stage_bytes;
+    // antenna-split all-gather fused into the epilogue (pnce_process_frames_gather): taps are
+    // laid out as the FULL [F][out_nr][n_t][L] CSI with this launch's receivers at rows
+    // out_r0.., written to `taps` and to every peer buffer in gather_dst (NVLink stores)
+    int32_t out_nr;       // receiver rows of the output layout (= n_r outside gather launches)
+    int32_t out_r0;       // first receiver row of this launch's slice (0 outside gather launches)
+    int32_t gather_n;     // peer buffers (0: none)
+    float* gather_dst[kMaxPeers];
     int32_t store_hint;   // L2 policy of the taps stores: 1 evict_first (default), 2 evict_last, 3 normal, 0 none
     int32_t raw_pol;      // L2 policy of the raw f32 row loads: 0 evict_first, 1 normal, 2 evict_last
     int32_t a_reuse;      // FusedTma, n_groups > 1: group 0 converts once and stores the fp16 A
@@ -407,7 +415,7 @@ __device__ __forceinline__ EpiLink make_link(const CorrParams& p, int64_t link) 
     e.f = f32;
     const int n_tx = min(p.n_batch, p.n_t - b * p.n_batch);
     e.n_valid = n_tx * p.l;
-    e.lbase = (e.f * p.n_r + r) * p.n_t + (int64_t)b * p.n_batch;
+    e.lbase = (e.f * p.out_nr + p.out_r0 + r) * p.n_t + (int64_t)b * p.n_batch;
     e.out = e.lbase * p.l;
     e.vec = (reinterpret_cast<uintptr_t>(p.taps + 2 * e.out) & 15) == 0;
     e.tvec = p.truth != nullptr && (reinterpret_cast<uintptr_t>(p.truth + 2 * e.out) & 15) == 0;
@@ -459,7 +467,7 @@ __device__ __forceinline__ void link_add(const CorrParams& p, const EpiLink& e, 
 
 // K4 for R repetitions of a 16x256b TMEM load: repetition i holds, for this thread's link,
 // Re (v[4i], v[4i+1]) and Im (v[4i+2], v[4i+3]) of lags n + 8i and n + 8i + 1.
-template <int R, bool SC>
+template <int R, bool SC, bool GA = false>
 __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v, const EpiLink& e, int n,
                                          float& s_abs, float& s_sq, float& nf, LinkAcc& la) {
 #pragma unroll
@@ -493,6 +501,17 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
                 *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
                 *reinterpret_cast<float2*>(dst + 2) = make_float2(re1, im1);
             }
+            if (GA) {
+                for (int d = 0; d < p.gather_n; ++d) {  // the same taps into every peer's CSI
+                    float* pd = p.gather_dst[d] + 2 * (e.out + lag);
+                    if (e.vec) {
+                        st_global_v4(pd, re0, im0, re1, im1);
+                    } else {
+                        *reinterpret_cast<float2*>(pd) = make_float2(re0, im0);
+                        *reinterpret_cast<float2*>(pd + 2) = make_float2(re1, im1);
+                    }
+                }
+            }
             if (SC && p.truth != nullptr) {
                 float4 h;
                 if (e.tvec) {
@@ -511,6 +530,9 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
             }
         } else {
             *reinterpret_cast<float2*>(dst) = make_float2(re0, im0);
+            if (GA)
+                for (int d = 0; d < p.gather_n; ++d)
+                    *reinterpret_cast<float2*>(p.gather_dst[d] + 2 * (e.out + lag)) = make_float2(re0, im0);
             if (SC && p.truth != nullptr) {
                 const float2 a = __ldg(reinterpret_cast<const float2*>(tr));
                 const float q0 = err_acc(re0, im0, a.x, a.y, s_abs, s_sq);
@@ -523,7 +545,7 @@ __device__ __forceinline__ void epi_reps(const CorrParams& p, const uint32_t* v,
 // Drain one 16-lane block (8 links) of the accumulator: TMEM -> x 1/M -> taps (+ scoring).
 // 64-column chunks double-buffered (the next chunk's TMEM load is in flight while the
 // current one is scaled and stored), then 16-column remainder pieces.
-template <bool SC>
+template <bool SC, bool GA = false>
 __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, const EpiLink& e, int n0,
                                           float& s_abs, float& s_sq, float& nf, int cols) {
     int c = 0;
@@ -535,13 +557,13 @@ __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, c
         while (true) {
             const bool more = c + 128 <= cols;
             if (more) tmem_ld_16x256b_x8(taddr + c + 64, vb);
-            epi_reps<8, SC>(p, va, e, n0 + c, s_abs, s_sq, nf, la);
+            epi_reps<8, SC, GA>(p, va, e, n0 + c, s_abs, s_sq, nf, la);
             c += 64;
             if (!more) break;
             tmem_wait_ld();
             const bool more2 = c + 128 <= cols;
             if (more2) tmem_ld_16x256b_x8(taddr + c + 64, va);
-            epi_reps<8, SC>(p, vb, e, n0 + c, s_abs, s_sq, nf, la);
+            epi_reps<8, SC, GA>(p, vb, e, n0 + c, s_abs, s_sq, nf, la);
             c += 64;
             if (!more2) break;
             tmem_wait_ld();
@@ -551,7 +573,7 @@ __device__ __forceinline__ void epi_block(const CorrParams& p, uint32_t taddr, c
         uint32_t v[8];
         tmem_ld_16x256b_x2(taddr + c, v);
         tmem_wait_ld();
-        epi_reps<2, SC>(p, v, e, n0 + c, s_abs, s_sq, nf, la);
+        epi_reps<2, SC, GA>(p, v, e, n0 + c, s_abs, s_sq, nf, la);
     }
     if (SC && p.link_err != nullptr) link_flush(p, e, la, false);
 }
@@ -845,7 +867,9 @@ __device__ __forceinline__ void t16_fold_mid(const CorrParams& p, uint32_t t_par
     tmem_wait_st();
 }
 
-template <int MODE, bool SCORED, bool EPI8 = false, bool T16 = false>
+// GATHER: plain launches whose epilogue also stores every tap into the peers' CSI buffers
+// (pnce_process_frames_gather; a separate instantiation so the other drains keep their registers)
+template <int MODE, bool SCORED, bool EPI8 = false, bool T16 = false, bool GATHER = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsK3, 1)
 k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_circ,
             const __grid_constant__ CUtensorMap tm_scr, const CorrParams p) {
@@ -1536,7 +1560,8 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #pragma unroll
                 for (int k = 0; k < kBlocksPerWarp; ++k) {
                     const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
-                    const bool ok = __all_sync(0xffffffffu, e.out >= 0 && e.vec && g * p.g_cols + p.g_cols <= e.n_valid);
+                    const bool ok = !GATHER && __all_sync(0xffffffffu, e.out >= 0 && e.vec &&
+                                                                         g * p.g_cols + p.g_cols <= e.n_valid);
                     fast_dst[k] = ok ? p.taps + 2 * (e.out + n0) : nullptr;
                 }
             }
@@ -1594,7 +1619,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                             epi_block_fast(p, taddr, fast_dst[k] + 2 * c0, nc);
                         } else {
                             const EpiLink e = make_link(p, link0 + 8 * bb);
-                            epi_block<false>(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
+                            epi_block<false, GATHER>(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
                         }
                     }
                     if (split && h == 0) {
@@ -2016,6 +2041,10 @@ static cudaError_t set_smem_attrs() {
     if (e == cudaSuccess && MODE == kModeFusedTma)
         e = cudaFuncSetAttribute(k_correlate<kModeFusedTma, false, true, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if constexpr (MODE == kModeFusedTma || MODE == kModeFusedLdg)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_correlate<MODE, false, false, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     return e;
 }
 
@@ -2029,6 +2058,12 @@ static void launch_k3(bool scored, int grid, size_t smem, cudaStream_t st, const
     // -5 % for the fused path (converters become the bottleneck); PNCE_TUNE_EPI8 overrides
     const int epi8_env = knobs().epi8;
     const bool epi8 = epi8_env < 0 ? MODE == kModePacked : epi8_env == 1;
+    if constexpr (MODE == kModeFusedTma || MODE == kModeFusedLdg) {
+        if (prm.gather_n > 0) {  // antenna-split gather (plain launches only)
+            k_correlate<MODE, false, false, false, true><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
+            return;
+        }
+    }
     if (scored && knobs().scored_epi == 4)
         k_correlate<MODE, true, false><<<grid, kThreadsK3, smem, st>>>(a, b, c, prm);
     else if (scored)
@@ -2387,6 +2422,9 @@ static pnce_status_t fill_params(const pnce_plan_t* p, const Tiling& t, bool fus
     prm.stats = stats;
     prm.n_frames = n_frames;
     prm.n_taps = n_frames * (int64_t)c.n_r * c.n_t * c.l;
+    prm.out_nr = c.n_r;
+    prm.out_r0 = 0;
+    prm.gather_n = 0;
     return PNCE_OK;
 }
 
@@ -2487,9 +2525,17 @@ struct T16Opts {
 struct BodyLayout {
     int stride;
 };
+// Antenna-split gather: the launch's receivers are rows [r0, r0 + n_r) of an n_r_total-row CSI
+struct GatherOpts {
+    float* const* peers;
+    int n_peers;
+    int n_r_total;
+    int r0;
+};
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                          double* stats, float* link_err, int64_t n_frames, void* stream,
-                                         const T16Opts* t16 = nullptr, const BodyLayout* bodies = nullptr);
+                                         const T16Opts* t16 = nullptr, const BodyLayout* bodies = nullptr,
+                                         const GatherOpts* gather = nullptr);
 
 pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                   double* stats, void* workspace, size_t workspace_bytes, int64_t n_frames,
@@ -2497,6 +2543,22 @@ pnce_status_t pnce_process_frames(const pnce_plan_t* p, const float* iq, float* 
     (void)workspace;
     (void)workspace_bytes;
     return process_frames_impl(p, iq, taps, truth, stats, nullptr, n_frames, stream);
+}
+
+pnce_status_t pnce_process_frames_gather(const pnce_plan_t* p, const float* iq, float* csi, float* const* peers,
+                                         int32_t n_peers, int32_t n_r_total, int32_t r0, int64_t n_frames,
+                                         void* stream) {
+    if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
+    if (n_peers < 0 || n_peers > kMaxPeers) return fail(PNCE_ERR_INVALID_CONFIG, "0..7 peer buffers");
+    if (n_peers > 0 && !peers) return fail(PNCE_ERR_DIMENSION, "null peer list");
+    for (int d = 0; d < n_peers; ++d)
+        if (!peers[d] || (reinterpret_cast<uintptr_t>(peers[d]) & 7) != (reinterpret_cast<uintptr_t>(csi) & 7) ||
+            ((reinterpret_cast<uintptr_t>(peers[d]) ^ reinterpret_cast<uintptr_t>(csi)) & 15))
+            return fail(PNCE_ERR_DIMENSION, "peer CSI buffers must share the local buffer's 16-byte alignment");
+    if (r0 < 0 || n_r_total < p->cfg.n_r || r0 + p->cfg.n_r > n_r_total)
+        return fail(PNCE_ERR_DIMENSION, "receiver slice [r0, r0 + n_r) outside [0, n_r_total)");
+    GatherOpts g{peers, n_peers, n_r_total, r0};
+    return process_frames_impl(p, iq, csi, nullptr, nullptr, nullptr, n_frames, stream, nullptr, nullptr, &g);
 }
 
 pnce_status_t pnce_process_frames_scored(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
@@ -2567,7 +2629,7 @@ pnce_status_t pnce_process_bodies_tensor16(const pnce_plan_t* p, const float* bo
 
 static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, float* taps, const float* truth,
                                          double* stats, float* link_err, int64_t n_frames, void* stream,
-                                         const T16Opts* t16, const BodyLayout* bodies) {
+                                         const T16Opts* t16, const BodyLayout* bodies, const GatherOpts* gather) {
     if (!p) return fail(PNCE_ERR_INVALID_CONFIG, "null plan");
     if (n_frames < 0) return fail(PNCE_ERR_DIMENSION, "n_frames < 0");
     if (n_frames == 0) return PNCE_OK;
@@ -2597,6 +2659,13 @@ static pnce_status_t process_frames_impl(const pnce_plan_t* p, const float* iq, 
     if (s != PNCE_OK) return s;
     prm.iq = iq;
     prm.link_err = link_err;
+    if (gather) {
+        prm.out_nr = gather->n_r_total;
+        prm.out_r0 = gather->r0;
+        prm.gather_n = gather->n_peers;
+        for (int d = 0; d < gather->n_peers; ++d) prm.gather_dst[d] = gather->peers[d];
+        prm.n_taps = n_frames * (int64_t)gather->n_r_total * p->cfg.n_t * p->cfg.l;
+    }
     if (bodies) {  // compact bodies: sample k of a link's body at row offset k
         prm.samples = bodies->stride;
         prm.c = 0;

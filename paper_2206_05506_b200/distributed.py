@@ -79,6 +79,54 @@ def allgather_csi(taps: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat([p[:, :c] for p, c in zip(parts, cnts)], dim=1).to(dev)
 
 
+class CsiGather:
+    """The antenna split with the CSI all-gather fused into the estimation epilogue
+    (PAPER.md:150-153): every rank allocates the full (F, n_r, n_t, L) CSI once, the ranks
+    exchange CUDA-IPC handles of it, and each rank's launch (`Correlator.process_gather`)
+    stores its receivers' taps straight into every rank's buffer -- NVLink stores from the
+    kernel instead of a separate all-gather.  `run` is asynchronous; `wait` synchronises the
+    stream and barriers the group, after which `csi` holds the gathered CSI on every rank."""
+
+    def __init__(self, corr, n_r_total: int, n_frames: int, group=None):
+        from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+
+        self.group = group
+        self.world = _world(group)
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.corr = corr
+        self.r0, r1 = antenna_shard(n_r_total, self.rank, self.world)
+        if r1 - self.r0 != corr.n_r:
+            raise DimensionMismatchError(f"rank {self.rank} owns {r1 - self.r0} receivers, its correlator {corr.n_r}")
+        if self.world > 8:
+            raise InvalidConfigError("the fused gather addresses at most 7 peers")
+        self.csi = torch.zeros((n_frames, n_r_total, corr.cfg.n_t, corr.cfg.l), dtype=torch.complex64,
+                               device=corr.device)
+        self.peers = []
+        if self.world > 1:
+            torch.cuda.synchronize(corr.device)
+            mine = reduce_tensor(self.csi)[1]
+            handles = [None] * self.world
+            dist.all_gather_object(handles, mine, group=group)
+            self.peers = [rebuild_cuda_tensor(*h) for i, h in enumerate(handles) if i != self.rank]
+
+    def run(self, iq_part: torch.Tensor) -> torch.Tensor:
+        return self.corr.process_gather(iq_part, self.csi, self.r0, self.peers)
+
+    def wait(self) -> torch.Tensor:
+        torch.cuda.synchronize(self.corr.device)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        return self.csi
+
+    def close(self) -> None:
+        """Release the peer mappings (every rank, before any of them exits)."""
+        self.peers = []
+        torch.cuda.synchronize(self.corr.device)
+        torch.cuda.ipc_collect()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+
 def reduce_frame_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
     """Antenna split: each rank's per-frame stats (F, 4) cover its receivers only; the
     all-reduced sum is the frame-set's {sum|e|, sum|e|^2, non-finite, saturations}."""

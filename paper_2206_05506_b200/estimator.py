@@ -213,6 +213,35 @@ class Correlator:
                 truth_ptr, stats_ptr, None, 0, n_frames, _stream_ptr(self.device)))
         return out, stats
 
+    def process_gather(self, iq: torch.Tensor, csi: torch.Tensor, r0: int, peers=()) -> torch.Tensor:
+        """Antenna split with the all-gather fused into the epilogue (pnce_process_frames_gather):
+        this correlator's n_r receivers are rows [r0, r0 + n_r) of ``csi`` (complex64
+        (F, n_r_total, n_t, L) on this device); every tap goes into ``csi`` and into each peer
+        buffer (``peers``: same-shape tensors or raw device pointers mapped into this context,
+        e.g. the other ranks' ``csi`` opened over CUDA IPC).  Asynchronous on the current
+        stream; the ranks order themselves (stream sync + barrier) before reading."""
+        iq, n_frames = self._check_iq(iq)
+        n_t, L = self.cfg.n_t, self.cfg.l
+        if csi.dim() != 4 or csi.shape[0] != n_frames or tuple(csi.shape[2:]) != (n_t, L) or \
+                csi.dtype != torch.complex64 or not csi.is_contiguous():
+            raise DimensionMismatchError("csi must be contiguous complex64 (F, n_r_total, n_t, L)")
+        _same_device(self.device, csi=csi)
+        n_r_total = int(csi.shape[1])
+        ptrs = []
+        for q in peers:
+            if isinstance(q, torch.Tensor):
+                if tuple(q.shape) != tuple(csi.shape) or q.dtype != csi.dtype or not q.is_contiguous():
+                    raise DimensionMismatchError("peer CSI buffers must match csi")
+                ptrs.append(q.data_ptr())
+            else:
+                ptrs.append(int(q))
+        arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().pnce_process_frames_gather(
+                self._plan, ctypes.c_void_p(iq.data_ptr()), ctypes.c_void_p(csi.data_ptr()), arr, len(ptrs),
+                n_r_total, int(r0), n_frames, _stream_ptr(self.device)))
+        return csi
+
     def process_scored(self, iq: torch.Tensor, truth: torch.Tensor, out: torch.Tensor | None = None,
                        stats: torch.Tensor | None = None, link_mse: torch.Tensor | None = None):
         """`process` with the fused per-link scoring (north star (4)): returns
