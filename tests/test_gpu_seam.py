@@ -210,3 +210,28 @@ def test_graph_capture_replays_the_fused_launch(dev):
     torch.cuda.synchronize(dev)
     want1, _ = corr.process(x)
     assert torch.equal(out, want1) and not torch.equal(want0, want1)
+
+
+def test_gather_launch_writes_every_buffer(dev):
+    """pnce_process_frames_gather in one process: a correlator for receivers [16, 40) of a
+    64-receiver cfg3 writes its slice into the local CSI and into two more "peer" buffers
+    (plain device pointers), rows r0.. of the full layout, bit-identical to the full
+    correlator's rows; nothing else is touched.  Bad slices are rejected."""
+    cfg = P.PilotConfig(m=1023, c=64, n_t=64, n_batch=8, l=64, f_s=10e6)
+    from paper_2206_05506_b200 import synth as S
+    full = P.Correlator(P.default_spec(10), cfg, 64, device=dev)
+    h = S.draw_channel(full, 3, seed=5)
+    iq = S.simulate_frames(full, h, 10.0, seed=6)
+    ref, _ = full.process(iq)
+    r0, r1 = 16, 40
+    part = P.Correlator(P.default_spec(10), cfg, r1 - r0, device=dev)
+    bufs = [torch.full((3, 64, 64, 64), 7 + 7j, dtype=torch.complex64, device=dev) for _ in range(3)]
+    part.process_gather(iq[:, :, r0:r1].contiguous(), bufs[0], r0, peers=bufs[1:])
+    torch.cuda.synchronize(dev)
+    for b in bufs:
+        assert torch.equal(b[:, r0:r1], ref[:, r0:r1])
+        assert bool((b[:, :r0] == 7 + 7j).all()) and bool((b[:, r1:] == 7 + 7j).all())
+    with pytest.raises(P.DimensionMismatchError):
+        part.process_gather(iq[:, :, r0:r1].contiguous(), bufs[0], 48, peers=bufs[1:])   # rows 48..72 > 64
+    with pytest.raises(P.InvalidConfigError):
+        part.process_gather(iq[:, :, r0:r1].contiguous(), bufs[0], r0, peers=[bufs[1]] * 8)

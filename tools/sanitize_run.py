@@ -40,6 +40,10 @@ def run(dev):
         ht = torch.empty(corr.taps_shape(F), dtype=torch.complex64).pin_memory()
         corr.process_host(hi, ht, chunk=2)
         S.simulate_frames(corr, h, math.inf)
+        if n >= 4:  # the fused antenna gather: half the receivers into two full-CSI buffers
+            part = P.Correlator(P.default_spec((m + 1).bit_length() - 1), cfg, n // 2, device=dev)
+            bufs = [torch.zeros(corr.taps_shape(F), dtype=torch.complex64, device=dev) for _ in range(2)]
+            part.process_gather(iq[:, :, n // 2:].contiguous(), bufs[0], n // 2, peers=bufs[1:])
     rows = np.sign(np.random.default_rng(0).standard_normal((40, 255)))
     y = np.random.default_rng(1).standard_normal((255, 3)) + 1j
     P.correlate_rows(rows, y)
