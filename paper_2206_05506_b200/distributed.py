@@ -107,7 +107,27 @@ class CsiGather:
             mine = reduce_tensor(self.csi)[1]
             handles = [None] * self.world
             dist.all_gather_object(handles, mine, group=group)
-            self.peers = [rebuild_cuda_tensor(*h) for i, h in enumerate(handles) if i != self.rank]
+            # open the peers' buffers; every rank must succeed (and reach each peer's device
+            # directly) before any kernel stores into them -- agreed collectively, so all
+            # ranks either proceed or raise together
+            err = ""
+            try:
+                me = corr.device.index
+                for i, h in enumerate(handles):
+                    if i == self.rank:
+                        continue
+                    pdev = torch.device(h[6]).index if not isinstance(h[6], int) else h[6]
+                    if pdev != me and not torch.cuda.can_device_access_peer(me, pdev):
+                        raise InvalidConfigError(f"cuda:{me} cannot access cuda:{pdev} directly")
+                    self.peers.append(rebuild_cuda_tensor(*h))
+            except Exception as exc:  # noqa: BLE001 -- reported collectively below
+                err = f"rank {self.rank}: {type(exc).__name__}: {exc}"
+            errs = [None] * self.world
+            dist.all_gather_object(errs, err, group=group)
+            bad = [e for e in errs if e]
+            if bad:
+                self.peers = []
+                raise InvalidConfigError("fused CSI gather unavailable: " + bad[0])
 
     def run(self, iq_part: torch.Tensor) -> torch.Tensor:
         return self.corr.process_gather(iq_part, self.csi, self.r0, self.peers)
