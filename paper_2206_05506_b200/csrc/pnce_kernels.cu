@@ -738,8 +738,16 @@ __device__ __forceinline__ void epi_reps_fast(const uint32_t* v, float* dst, flo
     }
 }
 
+template <bool GA = false>
 __device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t taddr, float* dst, int cols) {
     const float s = p.inv_m;
+    // GA: the same registers also go to every peer's CSI (same offset in each buffer)
+    const int64_t off = dst - p.taps;
+    auto emit = [&](const uint32_t* v, int c, int reps, uint64_t pol) {
+        epi_reps_fast(v, dst + 2 * c, s, reps, pol);
+        if constexpr (GA)
+            for (int d = 0; d < p.gather_n; ++d) epi_reps_fast(v, p.gather_dst[d] + off + 2 * c, s, reps, pol);
+    };
     PNCE_CHECK(dst >= p.taps && dst + 2 * cols - 12 <= p.taps + 2 * p.n_taps);  // last 16-byte store of the thread
     const uint64_t pol = p.store_hint == 1   ? policy_evict_first()
                          : p.store_hint == 2 ? policy_evict_last()
@@ -753,13 +761,13 @@ __device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t tad
         while (true) {
             const bool more = c + 128 <= cols;
             if (more) tmem_ld_16x256b_x8(taddr + c + 64, vb);
-            epi_reps_fast(va, dst + 2 * c, s, 8, pol);
+            emit(va, c, 8, pol);
             c += 64;
             if (!more) break;
             tmem_wait_ld();
             const bool more2 = c + 128 <= cols;
             if (more2) tmem_ld_16x256b_x8(taddr + c + 64, va);
-            epi_reps_fast(vb, dst + 2 * c, s, 8, pol);
+            emit(vb, c, 8, pol);
             c += 64;
             if (!more2) break;
             tmem_wait_ld();
@@ -769,7 +777,7 @@ __device__ __forceinline__ void epi_block_fast(const CorrParams& p, uint32_t tad
         uint32_t v[8];
         tmem_ld_16x256b_x2(taddr + c, v);
         tmem_wait_ld();
-        epi_reps_fast(v, dst + 2 * c, s, 2, pol);
+        emit(v, c, 2, pol);
     }
 }
 
@@ -1560,8 +1568,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
 #pragma unroll
                 for (int k = 0; k < kBlocksPerWarp; ++k) {
                     const EpiLink e = make_link(p, link0 + 8 * (bb0 + k));
-                    const bool ok = !GATHER && __all_sync(0xffffffffu, e.out >= 0 && e.vec &&
-                                                                         g * p.g_cols + p.g_cols <= e.n_valid);
+                    const bool ok = __all_sync(0xffffffffu, e.out >= 0 && e.vec && g * p.g_cols + p.g_cols <= e.n_valid);
                     fast_dst[k] = ok ? p.taps + 2 * (e.out + n0) : nullptr;
                 }
             }
@@ -1616,7 +1623,7 @@ k_correlate(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ C
                         const uint32_t taddr = t_acc + ((uint32_t)(quarter * 32 + 16 * bb) << 16) + (uint32_t)c0;
                         // warp-uniform choice (tcgen05.ld is .sync.aligned): every lane's run covers the tile
                         if (fast_dst[k] != nullptr) {
-                            epi_block_fast(p, taddr, fast_dst[k] + 2 * c0, nc);
+                            epi_block_fast<GATHER>(p, taddr, fast_dst[k] + 2 * c0, nc);
                         } else {
                             const EpiLink e = make_link(p, link0 + 8 * bb);
                             epi_block<false, GATHER>(p, taddr, e, n0 + c0, s_abs[k], s_sq[k], nf[k], nc);
