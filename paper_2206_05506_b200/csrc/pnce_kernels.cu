@@ -2559,8 +2559,7 @@ pnce_status_t pnce_process_frames_gather(const pnce_plan_t* p, const float* iq, 
     if (n_peers < 0 || n_peers > kMaxPeers) return fail(PNCE_ERR_INVALID_CONFIG, "0..7 peer buffers");
     if (n_peers > 0 && !peers) return fail(PNCE_ERR_DIMENSION, "null peer list");
     for (int d = 0; d < n_peers; ++d)
-        if (!peers[d] || (reinterpret_cast<uintptr_t>(peers[d]) & 7) != (reinterpret_cast<uintptr_t>(csi) & 7) ||
-            ((reinterpret_cast<uintptr_t>(peers[d]) ^ reinterpret_cast<uintptr_t>(csi)) & 15))
+        if (!peers[d] || ((reinterpret_cast<uintptr_t>(peers[d]) ^ reinterpret_cast<uintptr_t>(csi)) & 15))
             return fail(PNCE_ERR_DIMENSION, "peer CSI buffers must share the local buffer's 16-byte alignment");
     if (r0 < 0 || n_r_total < p->cfg.n_r || r0 + p->cfg.n_r > n_r_total)
         return fail(PNCE_ERR_DIMENSION, "receiver slice [r0, r0 + n_r) outside [0, n_r_total)");
